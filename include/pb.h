@@ -1,0 +1,234 @@
+/*
+ * pb.h -- C ABI of libpb, the B200 (sm_100a) PrecisionBatching bitlayer
+ * matvec / skinny-matmul library.
+ *
+ * Paper: "PrecisionBatching", arXiv 2003.00822 (/root/reference/PAPER.md,
+ * cited "P:<line>").  The library implements the inference stage (Alg. 2,
+ * P:183-202) on the GPU and the preprocessing stage (Alg. 1) on
+ * the host.  Numerical readings of the paper (tie rules, activation scaling,
+ * layouts, ...) are the G1..G16 entries of DESIGN.md "Readings".
+ *
+ * Conventions for every entry point
+ *   - Plain C types only.  Device pointers are raw CUDA device addresses;
+ *     `pb_stream` is a cudaStream_t passed as an opaque pointer (NULL = the
+ *     legacy default stream).
+ *   - Ownership: the caller allocates every buffer (packed weights,
+ *     workspace, x, y, acc).  Nothing in pb_matmul* allocates or frees device
+ *     memory and nothing synchronises the host; calls are stream-ordered and
+ *     CUDA-graph capturable.  The only library-owned object is pb_comm.
+ *   - Errors: arguments are validated before any launch.  A non-OK status
+ *     leaves outputs untouched and sets a thread-local message readable with
+ *     pb_last_error().  Launch failures map to PB_ECUDA; device faults
+ *     surface at the caller's next synchronisation.  No exceptions cross the
+ *     ABI; the library never prints or exits.
+ *   - There is no CPU fallback: every compute entry point runs CUDA kernels
+ *     and fails with PB_ECUDA when no device is usable.
+ */
+#ifndef PB_H_
+#define PB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PB_OK = 0,
+    PB_EINVAL = 1,      /* bad argument: null/misaligned pointer, out-of-range size or knob */
+    PB_ERANGE = 2,      /* int64 accumulator bound (reading G11) or a code out of range     */
+    PB_EDEGENERATE = 3, /* informational: max(W) == min(W); a valid pack was still written  */
+    PB_ECUDA = 4,       /* CUDA runtime error (no device, launch failure, ...)              */
+    PB_ENCCL = 5        /* NCCL unavailable or failed                                       */
+} pb_status;
+
+typedef void* pb_stream;
+
+/* Weight quantisation modes for pb_quantize_pack_weights (Alg. 1). */
+enum {
+    PB_Q_GRID = 0,    /* default: code = clamp(rint(W/d)), d = (max-min)/2^(L-1), s_w = d (G1, G3) */
+    PB_Q_ALG1 = 1,    /* literal Alg. 1: W_q = trunc(Q(W)*2^16), max_bit window, floor (G2, G3)  */
+    PB_Q_BINARY = 2   /* 1-bit +-v code, v = mean|W| (G7); requires layers == 1          */
+};
+
+/* act_frac value selecting the per-column power-of-two fixed point (G8). */
+#define PB_ACT_AUTO (-1024)
+
+/* Epilogue functions for pb_linear (applied in fp32 after the bias). */
+enum { PB_FN_NONE = 0, PB_FN_RELU = 1, PB_FN_TANH = 2, PB_FN_SIGMOID = 3 };
+
+/* Kernel engine for the binary product (step a3).  AUTO picks per shape. */
+enum { PB_ENGINE_AUTO = 0, PB_ENGINE_POPC = 1, PB_ENGINE_MMA = 2 };
+
+/*
+ * Packed weight bitlayers (D1).  Plain descriptor; `bits` is
+ * caller-owned memory (host or device) holding
+ *     bits[layer][row][kwords]   uint32 words, 16-byte aligned rows,
+ * layer 0 = the sign layer, layer i holds bit (L-1-i) of the
+ * L-bit two's-complement code; bit j of word w <-> column 32*w + j; padding
+ * columns are zero (AND-neutral).  kwords = 4*ceil(cols/128).
+ * Represented weight: W ~= scale * (sum_i S_i * W_i + offset) with
+ * S_0 = -2^(L-1) (or -2 when offset = 1, binary mode) and S_i = 2^(L-1-i).
+ */
+typedef struct {
+    uint32_t* bits;
+    int64_t rows, cols, kwords;
+    int32_t layers;   /* L, 1..16 */
+    int32_t offset;   /* o: 0, or 1 for the binary +-v code (L = 1)    */
+    double scale;     /* s_w: value of one code LSB                    */
+} pb_weights;
+
+/* Thread-local description of the last non-OK status ("" if none). */
+const char* pb_last_error(void);
+const char* pb_version(void);
+
+/* kwords = 4*ceil(cols/128) (16-byte row pitch). */
+int64_t pb_kwords(int64_t cols);
+
+/* Bytes of a packed [layers][rows][kwords] buffer (P:124 memory model:
+ * layers*rows*cols/8 algorithmic, plus row padding). */
+size_t pb_packed_bytes(int64_t rows, int64_t cols, int32_t layers);
+
+/*
+ * Offline preprocessing, Alg. 1 and §3.3.  Host code,
+ * double precision, no GPU needed when dst_is_device == 0.
+ *   W_host      [rows][cols] float32, row-major, host memory.
+ *   layers      L = stored bitlayers (1..16); PB_Q_GRID/ALG1 need L >= 2,
+ *               PB_Q_BINARY needs L == 1 (reading G1).
+ *   clip        > 0: clamp W to [-clip, clip] first; <= 0: none.
+ *   dst         pb_packed_bytes(rows, cols, layers) bytes, 16-byte aligned;
+ *               device memory if dst_is_device (copied on stream s, which
+ *               is synchronised before return: this call is offline).
+ *   out         filled descriptor (bits = dst).
+ * Returns PB_EDEGENERATE (with a valid zero/+-1 pack) when max(W) == min(W).
+ */
+pb_status pb_quantize_pack_weights(const float* W_host, int64_t rows, int64_t cols,
+                                   int32_t layers, int32_t quant_mode, float clip,
+                                   void* dst, int32_t dst_is_device, pb_stream s,
+                                   pb_weights* out);
+
+/* PB_Q_GRID with a caller-provided grid step d (> 0): code =
+ * clamp(rint(W/d)), scale = d.  Used to pack the row shards of one layer on
+ * several ranks with the layer's global d = (max(W) - min(W)) / 2^(L-1), so
+ * every shard carries exactly the codes of the unsharded layer (§8(e)). */
+pb_status pb_quantize_pack_weights_step(const float* W_host, int64_t rows, int64_t cols,
+                                        int32_t layers, double step, void* dst,
+                                        int32_t dst_is_device, pb_stream s, pb_weights* out);
+
+/* Pack caller-supplied integer codes [rows][cols] (L-bit two's complement;
+ * for offset = 1, L must be 1 and codes are +-1 meaning 1 - 2*bit).  Used by
+ * tests and by callers with their own quantiser.  PB_ERANGE if a code does
+ * not fit. */
+pb_status pb_pack_codes(const int32_t* codes_host, int64_t rows, int64_t cols,
+                        int32_t layers, int32_t offset, double scale,
+                        void* dst, int32_t dst_is_device, pb_stream s, pb_weights* out);
+
+/* Clip-threshold search (reading G6: 64 candidates (k/64)*max|W|,
+ * objective mean |s_w*code - W|, ties -> larger).  Host only, offline. */
+pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_t layers,
+                         float* clip_out);
+
+/*
+ * Workspace for the activation side of one call (steps a1-a2):
+ *   [f_b int32 x batch][x_q partial sums int64 x batch x 64][planes uint32
+ *   x batch x act_bits x kwords], each region 256-byte aligned.
+ */
+size_t pb_workspace_bytes(int64_t batch, int64_t cols, int32_t act_bits);
+
+/*
+ * Steps a1+a2: per batch column b, quantise x[b,:] to
+ * x_q = trunc(x * 2^f_b) (f_b per reading G8, or act_frac literal with
+ * saturation) and bit-transpose into act_bits planes (sign plane first) in
+ * the workspace.  x: device [batch][cols] float32.
+ */
+pb_status pb_act_quantize(const float* x, int64_t batch, int64_t cols, int32_t act_bits,
+                          int32_t act_frac, void* ws, size_t ws_bytes, pb_stream s);
+
+/*
+ * Steps a3-a5: for every output row r and
+ * batch column b, C_ij = popc(W_i[r,:] AND X_j[b,:]) for i < k_used, j < a,
+ *   acc = sum_i S_i sum_j T_j C_ij + offset * sum_c x_q[b,c]   (exact int64)
+ *   y   = fn( (float)ldexp((double)acc * scale, -f_b) + bias[r] (+ y_old) )
+ * reading the planes that pb_act_quantize left in ws.
+ *   y         device [batch][rows] float32 (required);
+ *   acc       device [batch][rows] int64 or NULL;
+ *   bias      device [rows] float32 or NULL;  fn: PB_FN_*;
+ *   accumulate  nonzero: add the previous contents of y before fn.
+ * k_used: weight bitlayers accumulated, 1..L, always the sign layer plus
+ * the most significant ones (reading G12).
+ */
+pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_weights* w,
+                     int32_t k_used,
+                     int32_t act_bits, float* y, int64_t* acc, const float* bias,
+                     int32_t fn, int32_t accumulate, pb_stream s);
+
+/* The whole hot path, Alg. 2: pb_act_quantize + pb_bitgemm (PB_FN_NONE,
+ * no bias).  y = W x in the paper's statement L_i(x) = Wx. */
+pb_status pb_matmul(const float* x, int64_t batch, const pb_weights* w, int32_t k_used,
+                    int32_t act_bits, int32_t act_frac, float* y, int64_t* acc,
+                    void* ws, size_t ws_bytes, pb_stream s);
+
+/* FC layer helper: y = fn(W x + bias) (P:256 MNIST FC layers). */
+pb_status pb_linear(const float* x, int64_t batch, const pb_weights* w, int32_t k_used,
+                    int32_t act_bits, int32_t act_frac, const float* bias, int32_t fn,
+                    float* y, void* ws, size_t ws_bytes, pb_stream s);
+
+/* Workspace for pb_rnn_step / pb_lstm_step: activation workspace for
+ * max(E, H) columns plus a [batch][gate_rows] float32 gate buffer. */
+size_t pb_cell_workspace_bytes(int64_t batch, int64_t in_cols, int64_t hidden,
+                               int32_t act_bits, int32_t gates);
+
+/* Elman RNN step (reading G15): h' = tanh(W_ih x + b_ih + W_hh h + b_hh).
+ * W_ih [H][E], W_hh [H][H]; x [batch][E], h, h_out [batch][H] (device). */
+pb_status pb_rnn_step(const float* x_t, const float* h, const pb_weights* w_ih,
+                      const pb_weights* w_hh, const float* b_ih, const float* b_hh,
+                      int32_t k_used_ih, int32_t k_used_hh, int32_t act_bits, int64_t batch,
+                      float* h_out, void* ws, size_t ws_bytes, pb_stream s);
+
+/* LSTM step (gate order i,f,g,o as PyTorch nn.LSTM, G15):
+ * gates = W_ih x + b_ih + W_hh h + b_hh, [batch][4H];
+ * c' = sigmoid(f) c + sigmoid(i) tanh(g);  h' = sigmoid(o) tanh(c').
+ * W_ih [4H][E], W_hh [4H][H] (device). */
+pb_status pb_lstm_step(const float* x_t, const float* h, const float* c,
+                       const pb_weights* w_ih, const pb_weights* w_hh,
+                       const float* b_ih, const float* b_hh, int32_t k_used_ih,
+                       int32_t k_used_hh, int32_t act_bits, int64_t batch,
+                       float* h_out, float* c_out, void* ws, size_t ws_bytes, pb_stream s);
+
+/* Select the binary-product engine (process-wide; default AUTO). */
+pb_status pb_set_engine(int32_t engine);
+int32_t pb_get_engine(void);
+
+/* ---------------- multi-GPU row sharding ----------------
+ * Rank g of N holds rows [row0, row0 + nrows) of every bitlayer, packed as
+ * its own pb_weights with rows = pb_shard_rows(...).  Balanced split:
+ * rows_per_rank = ceil(R/N); the last ranks may hold fewer (or zero) rows. */
+pb_status pb_shard_rows(int64_t rows_total, int32_t nranks, int32_t rank,
+                        int64_t* row0, int64_t* nrows);
+
+typedef struct pb_comm pb_comm;
+/* NCCL unique id (128 bytes) to broadcast from rank 0 (e.g. via
+ * torch.distributed).  NCCL is loaded at run time (libnccl.so.2). */
+pb_status pb_comm_unique_id(void* id128);
+pb_status pb_comm_init(pb_comm** comm, const void* id128, int32_t nranks, int32_t rank);
+pb_status pb_comm_destroy(pb_comm* comm);
+
+/* Extra workspace for pb_matmul_rowshard: gather buffer [N][batch][ceil(R/N)]. */
+size_t pb_rowshard_workspace_bytes(int64_t batch, int64_t cols, int32_t act_bits,
+                                   int64_t rows_total, int32_t nranks);
+
+/* Row-sharded y = W x: local pb_matmul on this rank's shard, then an NCCL
+ * all-gather of the y shards over NVLink on stream s, then (batch > 1 or
+ * uneven split) a permute into y_full [batch][rows_total].  x is replicated;
+ * every rank computes the same f_b and planes, so y_full is bit-identical to
+ * the single-GPU result. */
+pb_status pb_matmul_rowshard(const float* x, int64_t batch, const pb_weights* w_shard,
+                             int64_t rows_total, int32_t k_used, int32_t act_bits,
+                             int32_t act_frac, float* y_full, pb_comm* comm,
+                             void* ws, size_t ws_bytes, pb_stream s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PB_H_ */

@@ -1,0 +1,130 @@
+// pb_act.cu -- steps a1 + a2 of the hot path on sm_100a:
+//   a1 activation fixed-point cast  x_q = trunc(x * 2^f_b)   (Alg. 2 line 1, P:195;
+//      P:154 "a multiplication and a cast"; f_b per reading G8)
+//   a2 bitwise transpose of x_q into activation bitplanes
+// One warp turns 32 consecutive columns into `a` plane words with `a`
+// __ballot_sync votes (VOTE.ANY), sign plane first.  Σ_c x_q (needed only for
+// the binary-mode offset term) is produced as per-CTA partial sums.
+//
+// Grid: (nsplit, B) CTAs of 256 threads.  Every CTA recomputes max|x[b,:]|
+// (an L2-resident re-read of K floats) so no second launch or grid sync is
+// needed; it then transposes its own slice of words.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pb_common.cuh"
+#include "pb_internal.h"
+
+namespace pb {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kActAuto = -1024;   // == PB_ACT_AUTO
+
+__global__ void __launch_bounds__(kThreads)
+act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kwords, int a,
+                           int act_frac, int words_per_cta, int32_t* __restrict__ f_out,
+                           long long* __restrict__ xsum_part, uint32_t* __restrict__ planes)
+{
+    pdl_wait();          // x may be the previous kernel's output
+    pdl_trigger();       // let the dependent GEMV start its prologue
+
+    const int b = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* xb = x + (int64_t)b * K;
+
+    // ---- a1 (part 1): column max |x| (order-independent, exact) ----
+    float m = 0.f;
+    if ((K & 3) == 0 && ((reinterpret_cast<uintptr_t>(xb) & 15) == 0)) {
+        const float4* x4 = reinterpret_cast<const float4*>(xb);
+        for (int64_t c = tid; c < K / 4; c += kThreads) {
+            float4 v = __ldg(x4 + c);
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+    } else {
+        for (int64_t c = tid; c < K; c += kThreads) m = fmaxf(m, fabsf(__ldg(xb + c)));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float s_max[kWarps];
+    __shared__ long long s_sum[kWarps];
+    if (lane == 0) s_max[warp] = m;
+    __syncthreads();
+    m = s_max[0];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) m = fmaxf(m, s_max[w]);
+
+    int f;
+    if (act_frac == kActAuto) {
+        if (m == 0.f) {
+            f = 0;
+        } else {
+            int e;
+            frexpf(m, &e);           // m = frac * 2^e, frac in [0.5, 1): m < 2^e
+            f = (a - 1) - e;
+        }
+    } else {
+        f = act_frac;
+    }
+    if (blockIdx.x == 0 && tid == 0) f_out[b] = f;
+
+    // ---- a1 (part 2) + a2: cast, saturate, ballot-transpose ----
+    const double lo = -ldexp(1.0, a - 1), hi = ldexp(1.0, a - 1) - 1.0;
+    const int64_t w0 = (int64_t)blockIdx.x * words_per_cta;
+    int64_t w1 = w0 + words_per_cta;
+    if (w1 > kwords) w1 = kwords;
+    uint32_t* pb = planes + (int64_t)b * a * kwords;
+    long long xs = 0;
+    for (int64_t w = w0 + warp; w < w1; w += kWarps) {
+        const int64_t c = 32 * w + lane;
+        const float v = c < K ? __ldg(xb + c) : 0.f;
+        double t = ldexp((double)v, f);          // exact power-of-two scaling
+        t = fmin(fmax(t, lo), hi);               // saturation (literal act_frac only)
+        const long long q = __double2ll_rz(t);   // Int() = truncation toward zero
+        xs += q;
+        uint32_t mine = 0;
+        for (int j = 0; j < a; ++j) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (unsigned)((q >> (a - 1 - j)) & 1));
+            if (lane == j) mine = word;
+        }
+        if (lane < a) pb[(int64_t)lane * kwords + w] = mine;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+    if (lane == 0) s_sum[warp] = xs;
+    __syncthreads();
+    if (tid == 0) {
+        long long t = 0;
+        for (int w = 0; w < kWarps; ++w) t += s_sum[w];
+        xsum_part[(int64_t)b * kMaxSplit + blockIdx.x] = t;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kwords, int a,
+                             int act_frac, void* ws, cudaStream_t s)
+{
+    if (B == 0 || kwords == 0) return cudaSuccess;
+    const WsLayout l = ws_layout(B, kwords, a);
+    char* base = static_cast<char*>(ws);
+    const int nsplit = act_nsplit(kwords);
+    const int wpc = (int)((kwords + nsplit - 1) / nsplit);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nsplit, (unsigned)B, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, act_quant_transpose_kernel, x, K, kwords, a, act_frac, wpc,
+                              reinterpret_cast<int32_t*>(base + l.off_f),
+                              reinterpret_cast<long long*>(base + l.off_xsum),
+                              reinterpret_cast<uint32_t*>(base + l.off_planes));
+}
+
+}  // namespace pb

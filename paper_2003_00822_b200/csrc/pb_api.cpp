@@ -1,0 +1,680 @@
+// pb_api.cpp -- host side of libpb: the C ABI declared in include/pb.h.
+//   * argument validation (before any launch), thread-local error text;
+//   * the offline packer: Q(W) / Alg. 1 / binary
+//     +-v in double precision, then the L-bitlayer decomposition
+//      packed 32 columns per uint32 word;
+//   * kernel launches for the hot path (Alg. 2) and the layer
+//     helpers, all stream-ordered, no host sync, no allocation;
+//   * the row-shard all-gather over NCCL (loaded at run time).
+// Product code: shares nothing with oracle/.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "pb.h"
+#include "pb_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+int g_engine = PB_ENGINE_AUTO;
+
+pb_status fail(pb_status st, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+pb_status cuda_fail(cudaError_t e, const char* what) {
+    cudaGetLastError();   // clear the sticky-free error state
+    return fail(PB_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int ceil_log2(int64_t v) {
+    int k = 0;
+    while (((int64_t)1 << k) < v) ++k;
+    return k;
+}
+
+// ------------------------------------------------------------------ packer
+// Quantisers: double precision, FMA-free operation sequences (reading G13's
+// rule applied offline): grid  d = (max-min)/2^(L-1), code = clamp(rint(w/d)).
+struct QuantOut {
+    std::vector<int32_t> codes;
+    double scale = 1.0;
+    int offset = 0;
+    bool degenerate = false;
+};
+
+inline double clipv(double w, double clip) {
+    if (clip > 0) {
+        if (w > clip) w = clip;
+        if (w < -clip) w = -clip;
+    }
+    return w;
+}
+
+void minmax(const float* W, int64_t n, double clip, double& mn, double& mx) {
+    mx = -INFINITY;
+    mn = INFINITY;
+    for (int64_t e = 0; e < n; ++e) {
+        const double w = clipv((double)W[e], clip);
+        mx = w > mx ? w : mx;
+        mn = w < mn ? w : mn;
+    }
+}
+
+// Q(W) step d with the degenerate rule of reading G5.
+double grid_step(double mn, double mx, int n, bool& degenerate) {
+    double d = (mx - mn) / std::ldexp(1.0, n);
+    degenerate = false;
+    if (d == 0.0) {
+        degenerate = true;
+        d = std::fabs(mx);
+        if (d == 0.0) d = 1.0;
+    }
+    return d;
+}
+
+pb_status quantize_grid(const float* W, int64_t n, int L, double clip, QuantOut& q) {
+    double mn, mx;
+    minmax(W, n, clip, mn, mx);
+    bool deg;
+    const double d = grid_step(mn, mx, L - 1, deg);
+    const double lo = -std::ldexp(1.0, L - 1), hi = std::ldexp(1.0, L - 1) - 1.0;
+    q.codes.resize((size_t)n);
+    q.scale = d;
+    q.offset = 0;
+    q.degenerate = deg;
+    bool all_zero = deg && mx == 0.0 && mn == 0.0;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n; ++e) {
+        double m = std::rint(clipv((double)W[e], clip) / d);
+        m = m < lo ? lo : (m > hi ? hi : m);
+        q.codes[(size_t)e] = all_zero ? 0 : (int32_t)m;
+    }
+    if (all_zero) q.scale = 1.0;
+    return PB_OK;
+}
+
+pb_status quantize_alg1(const float* W, int64_t n, int L, double clip, QuantOut& q) {
+    // Alg. 1: W_q = Int(Q(W) * 2^16); max_bit = floor(log2 max|W_q|);
+    // keep bit positions max_bit+1 (sign) .. max_bit-n+1 (reading G2).
+    const int nb = L - 1;
+    double mn, mx;
+    minmax(W, n, clip, mn, mx);
+    bool deg;
+    const double d = grid_step(mn, mx, nb, deg);
+    std::vector<int64_t> wq((size_t)n);
+    int64_t maxabs = 0;
+    for (int64_t e = 0; e < n; ++e) {
+        const double Q = d * std::rint(clipv((double)W[e], clip) / d);
+        const double t = std::trunc(Q * 65536.0);
+        if (std::fabs(t) >= 9.0e18) return fail(PB_ERANGE, "Alg. 1: W_q overflows int64");
+        wq[(size_t)e] = (int64_t)t;
+        const int64_t a = wq[(size_t)e] < 0 ? -wq[(size_t)e] : wq[(size_t)e];
+        maxabs = a > maxabs ? a : maxabs;
+    }
+    q.codes.assign((size_t)n, 0);
+    q.offset = 0;
+    q.degenerate = deg;
+    if (maxabs == 0) {
+        q.scale = 1.0;
+        q.degenerate = true;
+        return PB_OK;
+    }
+    int max_bit = 63 - __builtin_clzll((unsigned long long)maxabs);
+    const int lo = max_bit - nb + 1;
+    for (int64_t e = 0; e < n; ++e) {
+        const int64_t v = wq[(size_t)e];
+        q.codes[(size_t)e] = (int32_t)(lo >= 0 ? (v >> lo) : (v * ((int64_t)1 << (-lo))));
+    }
+    q.scale = std::ldexp(1.0, lo - 16);
+    return PB_OK;
+}
+
+pb_status quantize_binary(const float* W, int64_t n, double clip, QuantOut& q) {
+    // P:152 1-bit +-v; v = mean|W| (reading G7); bit = [W < 0]; code 1 - 2*bit.
+    double s = 0.0;
+    q.codes.resize((size_t)n);
+    for (int64_t e = 0; e < n; ++e) {
+        const double w = clipv((double)W[e], clip);
+        s += std::fabs(w);
+        q.codes[(size_t)e] = w < 0.0 ? -1 : 1;
+    }
+    q.scale = s / (double)n;
+    q.offset = 1;
+    q.degenerate = false;
+    if (q.scale == 0.0) {
+        q.scale = 1.0;
+        q.degenerate = true;
+    }
+    return PB_OK;
+}
+
+// Decompose + pack: layer i = bit (L-1-i) of the L-bit two's-complement code
+// (binary mode: the single layer is [code == -1]).
+pb_status pack(const int32_t* codes, int64_t R, int64_t K, int L, int offset, std::vector<uint32_t>& out) {
+    const int64_t kw = pb_kwords(K);
+    out.assign((size_t)L * (size_t)R * (size_t)kw, 0u);
+    const int64_t lo = offset ? -1 : -((int64_t)1 << (L - 1));
+    const int64_t hi = offset ? 1 : ((int64_t)1 << (L - 1)) - 1;
+    int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+    for (int64_t r = 0; r < R; ++r) {
+        for (int64_t c = 0; c < K; ++c) {
+            const int32_t m = codes[r * K + c];
+            if (m < lo || m > hi || (offset && m == 0)) {
+                bad = 1;
+                continue;
+            }
+            const uint32_t u = offset ? (m == -1 ? 1u : 0u) : (uint32_t)m;
+            const uint32_t bit = 1u << (c & 31);
+            for (int i = 0; i < L; ++i)
+                if ((u >> (L - 1 - i)) & 1u) out[((size_t)i * R + r) * kw + (c >> 5)] |= bit;
+        }
+    }
+    if (bad) return fail(PB_ERANGE, "a code does not fit %d-bit two's complement%s", L,
+                         offset ? " (binary mode needs codes +-1)" : "");
+    return PB_OK;
+}
+
+pb_status store(const std::vector<uint32_t>& host, int64_t R, int64_t K, int L, int offset, double scale,
+                void* dst, int dst_is_device, pb_stream s, pb_weights* out) {
+    const size_t bytes = host.size() * sizeof(uint32_t);
+    if (dst_is_device) {
+        cudaStream_t st = static_cast<cudaStream_t>(s);
+        cudaError_t e = cudaMemcpyAsync(dst, host.data(), bytes, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "pack: copy to device");
+    } else if (bytes) {
+        std::memcpy(dst, host.data(), bytes);
+    }
+    out->bits = static_cast<uint32_t*>(dst);
+    out->rows = R;
+    out->cols = K;
+    out->kwords = pb_kwords(K);
+    out->layers = L;
+    out->offset = offset;
+    out->scale = scale;
+    return PB_OK;
+}
+
+// ------------------------------------------------------------------ launch
+pb_status check_weights(const pb_weights* w) {
+    if (!w) return fail(PB_EINVAL, "weights descriptor is NULL");
+    if (w->layers < 1 || w->layers > 16) return fail(PB_EINVAL, "layers=%d not in [1,16]", w->layers);
+    if (w->offset != 0 && !(w->offset == 1 && w->layers == 1))
+        return fail(PB_EINVAL, "offset=%d requires layers == 1 (binary mode)", w->offset);
+    if (w->rows < 0 || w->cols < 0) return fail(PB_EINVAL, "negative rows/cols");
+    if (w->kwords != pb_kwords(w->cols)) return fail(PB_EINVAL, "kwords=%lld != 4*ceil(cols/128)", (long long)w->kwords);
+    if (w->rows > 0 && w->kwords > 0 && (!w->bits || !aligned(w->bits, 16)))
+        return fail(PB_EINVAL, "bits must be a non-NULL 16-byte aligned device pointer");
+    return PB_OK;
+}
+
+pb_status check_act(int64_t batch, int64_t cols, int32_t a, int32_t act_frac) {
+    if (batch < 0 || batch > 65535) return fail(PB_EINVAL, "batch=%lld not in [0,65535]", (long long)batch);
+    if (cols < 0) return fail(PB_EINVAL, "cols < 0");
+    if (a < 1 || a > 32) return fail(PB_EINVAL, "act_bits=%d not in [1,32]", a);
+    if (act_frac != PB_ACT_AUTO && (act_frac < -126 || act_frac > 126))
+        return fail(PB_EINVAL, "act_frac=%d not PB_ACT_AUTO or in [-126,126]", act_frac);
+    return PB_OK;
+}
+
+pb_status check_ws(const void* ws, size_t ws_bytes, int64_t batch, int64_t cols, int32_t a) {
+    const size_t need = pb_workspace_bytes(batch, cols, a);
+    if (!ws || !aligned(ws, 16)) return fail(PB_EINVAL, "workspace must be non-NULL and 16-byte aligned");
+    if (ws_bytes < need) return fail(PB_EINVAL, "workspace %zu bytes < required %zu", ws_bytes, need);
+    return PB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pb_last_error(void) { return g_err; }
+const char* pb_version(void) { return "pbatch-b200 0.1 (sm_100a)"; }
+
+int64_t pb_kwords(int64_t cols) { return cols <= 0 ? 0 : 4 * ((cols + 127) / 128); }
+
+size_t pb_packed_bytes(int64_t rows, int64_t cols, int32_t layers) {
+    if (rows < 0 || cols < 0 || layers < 1) return 0;
+    return (size_t)layers * (size_t)rows * (size_t)pb_kwords(cols) * sizeof(uint32_t);
+}
+
+pb_status pb_quantize_pack_weights(const float* W_host, int64_t rows, int64_t cols, int32_t layers,
+                                   int32_t quant_mode, float clip, void* dst, int32_t dst_is_device,
+                                   pb_stream s, pb_weights* out) {
+    g_err[0] = 0;
+    if (!out) return fail(PB_EINVAL, "out is NULL");
+    if (rows < 0 || cols < 0) return fail(PB_EINVAL, "negative rows/cols");
+    if (rows * cols > 0 && !W_host) return fail(PB_EINVAL, "W_host is NULL");
+    if (pb_packed_bytes(rows, cols, layers) > 0 && (!dst || !aligned(dst, 16)))
+        return fail(PB_EINVAL, "dst must be non-NULL and 16-byte aligned");
+    if (quant_mode == PB_Q_BINARY) {
+        if (layers != 1) return fail(PB_EINVAL, "PB_Q_BINARY needs layers == 1");
+    } else if (quant_mode == PB_Q_GRID || quant_mode == PB_Q_ALG1) {
+        if (layers < 2 || layers > 16) return fail(PB_EINVAL, "layers=%d not in [2,16]", layers);
+    } else {
+        return fail(PB_EINVAL, "unknown quant_mode %d", quant_mode);
+    }
+    const int64_t n = rows * cols;
+    QuantOut q;
+    pb_status st = PB_OK;
+    if (n == 0) {
+        q.scale = 1.0;
+        q.offset = quant_mode == PB_Q_BINARY ? 1 : 0;
+        q.degenerate = true;
+    } else if (quant_mode == PB_Q_GRID) {
+        st = quantize_grid(W_host, n, layers, clip, q);
+    } else if (quant_mode == PB_Q_ALG1) {
+        st = quantize_alg1(W_host, n, layers, clip, q);
+    } else {
+        st = quantize_binary(W_host, n, clip, q);
+    }
+    if (st != PB_OK) return st;
+    std::vector<uint32_t> host;
+    if (n == 0) {
+        host.assign(pb_packed_bytes(rows, cols, layers) / 4, 0u);
+    } else if ((st = pack(q.codes.data(), rows, cols, layers, q.offset, host)) != PB_OK) {
+        return st;
+    }
+    st = store(host, rows, cols, layers, q.offset, q.scale, dst, dst_is_device, s, out);
+    if (st != PB_OK) return st;
+    if (q.degenerate) {
+        fail(PB_EDEGENERATE, "max(W) == min(W): degenerate grid (reading G5)");
+        return PB_EDEGENERATE;
+    }
+    return PB_OK;
+}
+
+pb_status pb_quantize_pack_weights_step(const float* W_host, int64_t rows, int64_t cols, int32_t layers,
+                                        double step, void* dst, int32_t dst_is_device, pb_stream s,
+                                        pb_weights* out) {
+    g_err[0] = 0;
+    if (!out) return fail(PB_EINVAL, "out is NULL");
+    if (rows < 0 || cols < 0) return fail(PB_EINVAL, "negative rows/cols");
+    if (rows * cols > 0 && !W_host) return fail(PB_EINVAL, "W_host is NULL");
+    if (layers < 2 || layers > 16) return fail(PB_EINVAL, "layers=%d not in [2,16]", layers);
+    if (!(step > 0.0) || !std::isfinite(step)) return fail(PB_EINVAL, "step must be finite and > 0");
+    if (pb_packed_bytes(rows, cols, layers) > 0 && (!dst || !aligned(dst, 16)))
+        return fail(PB_EINVAL, "dst must be non-NULL and 16-byte aligned");
+    const int64_t n = rows * cols;
+    const double lo = -std::ldexp(1.0, layers - 1), hi = std::ldexp(1.0, layers - 1) - 1.0;
+    std::vector<int32_t> codes((size_t)n);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < n; ++e) {
+        double m = std::rint((double)W_host[e] / step);
+        m = m < lo ? lo : (m > hi ? hi : m);
+        codes[(size_t)e] = (int32_t)m;
+    }
+    std::vector<uint32_t> host;
+    pb_status st = pack(codes.data(), rows, cols, layers, 0, host);
+    if (st != PB_OK) return st;
+    return store(host, rows, cols, layers, 0, step, dst, dst_is_device, s, out);
+}
+
+pb_status pb_pack_codes(const int32_t* codes_host, int64_t rows, int64_t cols, int32_t layers,
+                        int32_t offset, double scale, void* dst, int32_t dst_is_device, pb_stream s,
+                        pb_weights* out) {
+    g_err[0] = 0;
+    if (!out) return fail(PB_EINVAL, "out is NULL");
+    if (layers < 1 || layers > 16) return fail(PB_EINVAL, "layers=%d not in [1,16]", layers);
+    if (offset != 0 && !(offset == 1 && layers == 1)) return fail(PB_EINVAL, "offset needs layers == 1");
+    if (rows < 0 || cols < 0) return fail(PB_EINVAL, "negative rows/cols");
+    if (rows * cols > 0 && !codes_host) return fail(PB_EINVAL, "codes_host is NULL");
+    if (pb_packed_bytes(rows, cols, layers) > 0 && (!dst || !aligned(dst, 16)))
+        return fail(PB_EINVAL, "dst must be non-NULL and 16-byte aligned");
+    std::vector<uint32_t> host;
+    pb_status st = pack(codes_host, rows, cols, layers, offset, host);
+    if (st != PB_OK) return st;
+    return store(host, rows, cols, layers, offset, scale, dst, dst_is_device, s, out);
+}
+
+pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_t layers, float* clip_out) {
+    g_err[0] = 0;
+    if (!W_host || !clip_out || rows * cols <= 0) return fail(PB_EINVAL, "bad arguments");
+    if (layers < 2 || layers > 16) return fail(PB_EINVAL, "layers=%d not in [2,16]", layers);
+    const int64_t n = rows * cols;
+    double mx = 0.0;
+    for (int64_t e = 0; e < n; ++e) mx = std::fabs((double)W_host[e]) > mx ? std::fabs((double)W_host[e]) : mx;
+    if (mx == 0.0) {
+        *clip_out = 0.f;
+        return fail(PB_EDEGENERATE, "all-zero W");
+    }
+    constexpr int kCand = 64;
+    double best = INFINITY;
+    float best_t = (float)mx;
+    QuantOut q;
+    for (int k = 1; k <= kCand; ++k) {
+        const float t = (float)((double)k / (double)kCand * mx);
+        quantize_grid(W_host, n, layers, (double)t, q);
+        double err = 0.0;
+        for (int64_t e = 0; e < n; ++e) err += std::fabs(q.scale * (double)q.codes[(size_t)e] - (double)W_host[e]);
+        err /= (double)n;
+        if (err <= best) {
+            best = err;
+            best_t = t;
+        }
+    }
+    *clip_out = best_t;
+    return PB_OK;
+}
+
+size_t pb_workspace_bytes(int64_t batch, int64_t cols, int32_t act_bits) {
+    if (batch < 0 || cols < 0 || act_bits < 1 || act_bits > 32) return 0;
+    return pb::ws_layout(batch, pb_kwords(cols), act_bits).total;
+}
+
+pb_status pb_act_quantize(const float* x, int64_t batch, int64_t cols, int32_t act_bits, int32_t act_frac,
+                          void* ws, size_t ws_bytes, pb_stream s) {
+    g_err[0] = 0;
+    pb_status st = check_act(batch, cols, act_bits, act_frac);
+    if (st != PB_OK) return st;
+    if ((st = check_ws(ws, ws_bytes, batch, cols, act_bits)) != PB_OK) return st;
+    if (batch * cols > 0 && (!x || !aligned(x, 4))) return fail(PB_EINVAL, "x must be a non-NULL device pointer");
+    cudaError_t e = pb::launch_act_quant(x, batch, cols, pb_kwords(cols), act_bits, act_frac, ws,
+                                         static_cast<cudaStream_t>(s));
+    if (e != cudaSuccess) return cuda_fail(e, "act_quant_transpose launch");
+    return PB_OK;
+}
+
+static pb_status validate_gemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_weights* w,
+                               int32_t k_used, int32_t act_bits, const float* y, const int64_t* acc,
+                               int32_t fn) {
+    pb_status st = check_weights(w);
+    if (st != PB_OK) return st;
+    if ((st = check_act(batch, w->cols, act_bits, PB_ACT_AUTO)) != PB_OK) return st;
+    if ((st = check_ws(ws, ws_bytes, batch, w->cols, act_bits)) != PB_OK) return st;
+    if (k_used < 1 || k_used > w->layers) return fail(PB_EINVAL, "k_used=%d not in [1,%d]", k_used, w->layers);
+    if (fn < PB_FN_NONE || fn > PB_FN_SIGMOID) return fail(PB_EINVAL, "fn=%d unknown", fn);
+    if (batch * w->rows > 0 && (!y || !aligned(y, 4))) return fail(PB_EINVAL, "y must be a non-NULL device pointer");
+    if (acc && !aligned(acc, 8)) return fail(PB_EINVAL, "acc must be 8-byte aligned");
+    // reading G11: |acc| <= K 2^(L-1) 2^(a-1) (+ K 2^(a-1) for the offset) < 2^63
+    const int bound = ceil_log2(w->cols > 1 ? w->cols : 1) + w->layers + act_bits - 2 + (w->offset ? 1 : 0);
+    if (bound > 62) return fail(PB_ERANGE, "accumulator bound 2^%d exceeds int64 (reading G11)", bound + 1);
+    return PB_OK;
+}
+
+pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_weights* w, int32_t k_used,
+                     int32_t act_bits, float* y, int64_t* acc, const float* bias, int32_t fn,
+                     int32_t accumulate, pb_stream s) {
+    g_err[0] = 0;
+    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, fn);
+    if (st != PB_OK) return st;
+    if (batch == 0 || w->rows == 0) return PB_OK;
+
+    const pb::WsLayout l = pb::ws_layout(batch, w->kwords, act_bits);
+    const char* base = static_cast<const char*>(ws);
+    pb::GemmArgs g;
+    g.bits = w->bits;
+    g.R = w->rows;
+    g.kwords = w->kwords;
+    g.L = w->layers;
+    g.offset = w->offset;
+    g.k_used = k_used;
+    g.a = act_bits;
+    g.scale = w->scale;
+    g.planes = reinterpret_cast<const uint32_t*>(base + l.off_planes);
+    g.f = reinterpret_cast<const int32_t*>(base + l.off_f);
+    g.xsum = reinterpret_cast<const long long*>(base + l.off_xsum);
+    g.nsplit = pb::act_nsplit(w->kwords);
+    g.B = batch;
+    g.y = y;
+    g.acc = reinterpret_cast<long long*>(acc);
+    g.bias = bias;
+    g.fn = fn;
+    g.accumulate = accumulate ? 1 : 0;
+
+    cudaError_t e;
+    const cudaStream_t cs = static_cast<cudaStream_t>(s);
+    if (g_engine == PB_ENGINE_MMA) {
+        if (!pb::mma_supported(g)) return fail(PB_EINVAL, "PB_ENGINE_MMA does not support this shape");
+        e = pb::launch_gemm_mma(g, cs);
+    } else if (g_engine == PB_ENGINE_AUTO && pb::mma_supported(g)) {
+        e = pb::launch_gemm_mma(g, cs);
+    } else {
+        e = pb::launch_gemv_popc(g, cs);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "bitgemm launch");
+    return PB_OK;
+}
+
+pb_status pb_matmul(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
+                    int32_t act_frac, float* y, int64_t* acc, void* ws, size_t ws_bytes, pb_stream s) {
+    g_err[0] = 0;
+    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, PB_FN_NONE);
+    if (st != PB_OK) return st;
+    if ((st = check_act(batch, w->cols, act_bits, act_frac)) != PB_OK) return st;
+    if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
+    return pb_bitgemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, nullptr, PB_FN_NONE, 0, s);
+}
+
+pb_status pb_linear(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
+                    int32_t act_frac, const float* bias, int32_t fn, float* y, void* ws, size_t ws_bytes,
+                    pb_stream s) {
+    g_err[0] = 0;
+    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, nullptr, fn);
+    if (st != PB_OK) return st;
+    if ((st = check_act(batch, w->cols, act_bits, act_frac)) != PB_OK) return st;
+    if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
+    return pb_bitgemm(ws, ws_bytes, batch, w, k_used, act_bits, y, nullptr, bias, fn, 0, s);
+}
+
+size_t pb_cell_workspace_bytes(int64_t batch, int64_t in_cols, int64_t hidden, int32_t act_bits, int32_t gates) {
+    const int64_t k = in_cols > hidden ? in_cols : hidden;
+    const size_t a = pb_workspace_bytes(batch, k, act_bits);
+    return pb::align_up(a) + pb::align_up(sizeof(float) * (size_t)batch * (size_t)gates * (size_t)hidden);
+}
+
+static pb_status cell_common(const float* x_t, const float* h, const pb_weights* w_ih, const pb_weights* w_hh,
+                             const float* b_ih, const float* b_hh, int32_t k_ih, int32_t k_hh, int32_t a,
+                             int64_t batch, int gates, void* ws, size_t ws_bytes, pb_stream s, float** gbuf) {
+    pb_status st;
+    if ((st = check_weights(w_ih)) != PB_OK) return st;
+    if ((st = check_weights(w_hh)) != PB_OK) return st;
+    const int64_t H = w_hh->cols;
+    if (w_ih->rows != gates * H || w_hh->rows != gates * H)
+        return fail(PB_EINVAL, "W_ih/W_hh must have %d*H rows (H = W_hh cols = %lld)", gates, (long long)H);
+    const size_t need = pb_cell_workspace_bytes(batch, w_ih->cols, H, a, gates);
+    if (!ws || !aligned(ws, 16) || ws_bytes < need) return fail(PB_EINVAL, "cell workspace %zu < %zu", ws_bytes, need);
+    const int64_t k = w_ih->cols > H ? w_ih->cols : H;
+    const size_t act_ws = pb::align_up(pb_workspace_bytes(batch, k, a));
+    *gbuf = reinterpret_cast<float*>(static_cast<char*>(ws) + act_ws);
+    // gates = (W_ih x + b_ih), then gates = (W_hh h + b_hh) + gates
+    if ((st = pb_act_quantize(x_t, batch, w_ih->cols, a, PB_ACT_AUTO, ws, act_ws, s)) != PB_OK) return st;
+    if ((st = pb_bitgemm(ws, act_ws, batch, w_ih, k_ih, a, *gbuf, nullptr, b_ih, PB_FN_NONE, 0, s)) != PB_OK) return st;
+    if ((st = pb_act_quantize(h, batch, H, a, PB_ACT_AUTO, ws, act_ws, s)) != PB_OK) return st;
+    return pb_bitgemm(ws, act_ws, batch, w_hh, k_hh, a, *gbuf, nullptr, b_hh, PB_FN_NONE, 1, s);
+}
+
+pb_status pb_rnn_step(const float* x_t, const float* h, const pb_weights* w_ih, const pb_weights* w_hh,
+                      const float* b_ih, const float* b_hh, int32_t k_used_ih, int32_t k_used_hh, int32_t act_bits,
+                      int64_t batch, float* h_out, void* ws, size_t ws_bytes, pb_stream s) {
+    g_err[0] = 0;
+    float* gates = nullptr;
+    pb_status st = cell_common(x_t, h, w_ih, w_hh, b_ih, b_hh, k_used_ih, k_used_hh, act_bits, batch, 1, ws,
+                               ws_bytes, s, &gates);
+    if (st != PB_OK) return st;
+    if (!h_out) return fail(PB_EINVAL, "h_out is NULL");
+    cudaError_t e = pb::launch_rnn_cell(gates, batch, w_hh->cols, h_out, static_cast<cudaStream_t>(s));
+    if (e != cudaSuccess) return cuda_fail(e, "rnn_cell launch");
+    return PB_OK;
+}
+
+pb_status pb_lstm_step(const float* x_t, const float* h, const float* c, const pb_weights* w_ih,
+                       const pb_weights* w_hh, const float* b_ih, const float* b_hh, int32_t k_used_ih,
+                       int32_t k_used_hh, int32_t act_bits, int64_t batch, float* h_out, float* c_out, void* ws,
+                       size_t ws_bytes, pb_stream s) {
+    g_err[0] = 0;
+    float* gates = nullptr;
+    pb_status st = cell_common(x_t, h, w_ih, w_hh, b_ih, b_hh, k_used_ih, k_used_hh, act_bits, batch, 4, ws,
+                               ws_bytes, s, &gates);
+    if (st != PB_OK) return st;
+    if (!h_out || !c_out || !c) return fail(PB_EINVAL, "c/h_out/c_out is NULL");
+    cudaError_t e = pb::launch_lstm_cell(gates, c, batch, w_hh->cols, h_out, c_out, static_cast<cudaStream_t>(s));
+    if (e != cudaSuccess) return cuda_fail(e, "lstm_cell launch");
+    return PB_OK;
+}
+
+pb_status pb_set_engine(int32_t engine) {
+    if (engine < PB_ENGINE_AUTO || engine > PB_ENGINE_MMA) return fail(PB_EINVAL, "engine=%d unknown", engine);
+    g_engine = engine;
+    return PB_OK;
+}
+int32_t pb_get_engine(void) { return g_engine; }
+
+// ------------------------------------------------------------ row sharding
+pb_status pb_shard_rows(int64_t rows_total, int32_t nranks, int32_t rank, int64_t* row0, int64_t* nrows) {
+    if (rows_total < 0 || nranks < 1 || rank < 0 || rank >= nranks || !row0 || !nrows)
+        return fail(PB_EINVAL, "bad shard arguments");
+    const int64_t rs = (rows_total + nranks - 1) / nranks;
+    int64_t r0 = rs * rank;
+    if (r0 > rows_total) r0 = rows_total;
+    int64_t n = rows_total - r0;
+    if (n > rs) n = rs;
+    *row0 = r0;
+    *nrows = n;
+    return PB_OK;
+}
+
+}  // extern "C"
+
+// NCCL is resolved at run time so that libpb loads (and the CPU tests run)
+// without it; when torch has already loaded libnccl.so.2 we reuse that copy.
+struct pb_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 0, rank = 0;
+};
+
+namespace {
+struct Nccl {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+Nccl& nccl() {
+    static Nccl n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+        n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+        n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+        n.AllGather = reinterpret_cast<decltype(n.AllGather)>(dlsym(h, "ncclAllGather"));
+        n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.AllGather && n.GetErrorString;
+    });
+    return n;
+}
+pb_status nccl_fail(ncclResult_t r, const char* what) {
+    return fail(PB_ENCCL, "%s: %s", what, nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error");
+}
+}  // namespace
+
+extern "C" {
+
+pb_status pb_comm_unique_id(void* id128) {
+    g_err[0] = 0;
+    if (!id128) return fail(PB_EINVAL, "id128 is NULL");
+    if (!nccl().ok) return fail(PB_ENCCL, "libnccl.so.2 not loadable");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(id128, &id, 128);
+    return PB_OK;
+}
+
+pb_status pb_comm_init(pb_comm** comm, const void* id128, int32_t nranks, int32_t rank) {
+    g_err[0] = 0;
+    if (!comm || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return fail(PB_EINVAL, "bad comm arguments");
+    if (!nccl().ok) return fail(PB_ENCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    pb_comm* c = new pb_comm;
+    ncclResult_t r = nccl().CommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return nccl_fail(r, "ncclCommInitRank");
+    }
+    c->nranks = nranks;
+    c->rank = rank;
+    *comm = c;
+    return PB_OK;
+}
+
+pb_status pb_comm_destroy(pb_comm* comm) {
+    if (!comm) return PB_OK;
+    if (comm->comm && nccl().ok) nccl().CommDestroy(comm->comm);
+    delete comm;
+    return PB_OK;
+}
+
+size_t pb_rowshard_workspace_bytes(int64_t batch, int64_t cols, int32_t act_bits, int64_t rows_total,
+                                   int32_t nranks) {
+    if (nranks < 1) return 0;
+    const int64_t rs = (rows_total + nranks - 1) / nranks;
+    return pb::align_up(pb_workspace_bytes(batch, cols, act_bits)) +
+           pb::align_up(sizeof(float) * (size_t)batch * (size_t)rs) +
+           pb::align_up(sizeof(float) * (size_t)batch * (size_t)rs * (size_t)nranks);
+}
+
+pb_status pb_matmul_rowshard(const float* x, int64_t batch, const pb_weights* w_shard, int64_t rows_total,
+                             int32_t k_used, int32_t act_bits, int32_t act_frac, float* y_full, pb_comm* comm,
+                             void* ws, size_t ws_bytes, pb_stream s) {
+    g_err[0] = 0;
+    if (!comm) return fail(PB_EINVAL, "comm is NULL");
+    pb_status st = check_weights(w_shard);
+    if (st != PB_OK) return st;
+    const int N = comm->nranks;
+    const int64_t rs = (rows_total + N - 1) / N;
+    if (w_shard->rows != rs)
+        return fail(PB_EINVAL, "shard rows %lld != ceil(R/N) = %lld (pad the last shards with zero rows)",
+                    (long long)w_shard->rows, (long long)rs);
+    const size_t need = pb_rowshard_workspace_bytes(batch, w_shard->cols, act_bits, rows_total, N);
+    if (!ws || !aligned(ws, 16) || ws_bytes < need) return fail(PB_EINVAL, "rowshard workspace %zu < %zu", ws_bytes, need);
+    if (batch * rows_total > 0 && !y_full) return fail(PB_EINVAL, "y_full is NULL");
+    const size_t act_ws = pb::align_up(pb_workspace_bytes(batch, w_shard->cols, act_bits));
+    char* base = static_cast<char*>(ws);
+    const cudaStream_t cs = static_cast<cudaStream_t>(s);
+    if (batch == 1 && rs * N == rows_total) {
+        // y_full is [R]: compute this rank's rows in place, all-gather in place.
+        float* mine = y_full + (int64_t)comm->rank * rs;
+        if ((st = pb_matmul(x, batch, w_shard, k_used, act_bits, act_frac, mine, nullptr, ws, act_ws, s)) != PB_OK)
+            return st;
+        ncclResult_t r = nccl().AllGather(mine, y_full, (size_t)rs, ncclFloat32, comm->comm, cs);
+        if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+        return PB_OK;
+    }
+    float* ylocal = reinterpret_cast<float*>(base + act_ws);
+    float* gathered = reinterpret_cast<float*>(base + act_ws + pb::align_up(sizeof(float) * (size_t)batch * rs));
+    if ((st = pb_matmul(x, batch, w_shard, k_used, act_bits, act_frac, ylocal, nullptr, ws, act_ws, s)) != PB_OK)
+        return st;
+    ncclResult_t r = nccl().AllGather(ylocal, gathered, (size_t)(batch * rs), ncclFloat32, comm->comm, cs);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+    cudaError_t e = pb::launch_permute_shards(gathered, batch, rs, N, rows_total, y_full, cs);
+    if (e != cudaSuccess) return cuda_fail(e, "permute launch");
+    return PB_OK;
+}
+
+}  // extern "C"

@@ -107,3 +107,22 @@ def codes(R: int, K: int, L: int, s: int) -> np.ndarray:
 def binary_codes(R: int, K: int, s: int) -> np.ndarray:
     rng = np.random.default_rng(s)
     return np.where(rng.uniform(size=(R, K)) < 0.5, 1, -1).astype(np.int32)
+
+
+def weights_rows(R: int, K: int, s: int, r0: int = 0, r1: int | None = None,
+                 block: int = 1024) -> np.ndarray:
+    """Rows [r0, r1) of a large N(0, 1/K) weight matrix generated in blocks of
+    `block` rows, block b drawn from default_rng([s, b]).  Every rank of a
+    row-sharded run can draw exactly its own rows of the same matrix."""
+    r1 = R if r1 is None else r1
+    out = np.empty((max(0, r1 - r0), K), dtype=np.float32)
+    scale = np.float32(1.0 / np.sqrt(K))
+    b0, b1 = r0 // block, (r1 + block - 1) // block
+    for b in range(b0, b1):
+        lo, hi = b * block, min(R, (b + 1) * block)
+        rng = np.random.default_rng([s, b])
+        blk = rng.standard_normal((hi - lo, K), dtype=np.float32) * scale
+        a0, a1 = max(lo, r0), min(hi, r1)
+        if a1 > a0:
+            out[a0 - r0:a1 - r0] = blk[a0 - lo:a1 - lo]
+    return out
