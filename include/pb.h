@@ -130,9 +130,16 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
                          float* clip_out);
 
 /*
- * Workspace for the activation side of one call (steps a1-a2):
- *   [f_b int32 x batch][x_q partial sums int64 x batch x 64][planes uint32
- *   x batch x act_bits x kwords], each region 256-byte aligned.
+ * Workspace of one call (batch columns of a layer with `cols` inputs):
+ *   [stream-K tile counters int32 x 8192]     zero on entry, left zero on exit
+ *   [tensor-engine partial-tile slots int64 x 160 x 2 x batch x 128]
+ *   [f_b int32 x batch][x_q partial sums int64 x batch x 64]
+ *   [planes uint32 x batch x act_bits x kwords]
+ *   [tensor-engine B operand tiles: kwords x N_pad x 32 bytes, N_pad = a*batch
+ *    padded to 8/16/32, present when a*batch <= 32]
+ * each region 256-byte aligned.  The workspace must be zero-filled before its
+ * first use (the counters); every other region is rewritten by each call, so
+ * one workspace serves calls of any shape, but not two calls concurrently.
  */
 size_t pb_workspace_bytes(int64_t batch, int64_t cols, int32_t act_bits);
 

@@ -189,10 +189,13 @@ class PackedWeights:
 
 
 class Workspace:
+    """Zero-filled device workspace (the stream-K tile counters must start at
+    zero; every call leaves them zero again)."""
+
     def __init__(self, nbytes, device="cuda"):
         import torch
         self.nbytes = int(nbytes)
-        self.buf = torch.empty(max(self.nbytes, 256), dtype=torch.uint8, device=device)
+        self.buf = torch.zeros(max(self.nbytes, 256), dtype=torch.uint8, device=device)
 
     @property
     def ptr(self):

@@ -5,8 +5,13 @@
 // One warp turns 32 consecutive columns into `a` plane words with `a`
 // __ballot_sync votes (VOTE.ANY), sign plane first.  Σ_c x_q (needed only for
 // the binary-mode offset term) is produced as per-CTA partial sums.
+// When the tensor engine is used (a*B <= 32) the kernel also emits, per
+// 32-column k-block, the MMA B operand tile (N_pad plane rows x 32 bytes,
+// K-major no-swizzle canonical layout): byte kk = 4r + q of plane row n holds
+// bit (8q + r) of that plane word shifted to 2^(7-r), so that against the
+// weight byte 2^r * w_bit (pb_gemm_tc.cu) every 0/1 product is exactly 128.
 //
-// Grid: (nsplit, B) CTAs of 256 threads.  Every CTA recomputes max|x[b,:]|
+// Grid: (nsplit, B) CTAs of 512 threads.  Every CTA recomputes max|x[b,:]|
 // (an L2-resident re-read of K floats) so no second launch or grid sync is
 // needed; it then transposes its own slice of words.
 #include <cstdint>
@@ -18,14 +23,15 @@
 namespace pb {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kActAuto = -1024;   // == PB_ACT_AUTO
 
 __global__ void __launch_bounds__(kThreads)
 act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kwords, int a,
                            int act_frac, int words_per_cta, int32_t* __restrict__ f_out,
-                           long long* __restrict__ xsum_part, uint32_t* __restrict__ planes)
+                           long long* __restrict__ xsum_part, uint32_t* __restrict__ planes,
+                           uint8_t* __restrict__ bexp, int npad)
 {
     pdl_wait();          // x may be the previous kernel's output
     pdl_trigger();       // let the dependent GEMV start its prologue
@@ -37,10 +43,19 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
     // ---- a1 (part 1): column max |x| (order-independent, exact) ----
     float m = 0.f;
     if ((K & 3) == 0 && ((reinterpret_cast<uintptr_t>(xb) & 15) == 0)) {
+        // issue 8 independent 128-bit loads per thread before using any
         const float4* x4 = reinterpret_cast<const float4*>(xb);
-        for (int64_t c = tid; c < K / 4; c += kThreads) {
-            float4 v = __ldg(x4 + c);
-            m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        const int64_t n4 = K / 4;
+        for (int64_t c0 = tid; c0 < n4; c0 += 8 * kThreads) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t c = c0 + (int64_t)u * kThreads;
+                v[u] = c < n4 ? __ldg(x4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
         }
     } else {
         for (int64_t c = tid; c < K; c += kThreads) m = fmaxf(m, fabsf(__ldg(xb + c)));
@@ -89,6 +104,32 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
             if (lane == j) mine = word;
         }
         if (lane < a) pb[(int64_t)lane * kwords + w] = mine;
+        if (npad) {
+            // B tile rows n = b*a + j; lane pair (j, half) writes 16 bytes:
+            // uint32 for r = 4*half + t holds bytes q = 0..3 = bit (8q + r) << (7 - r).
+            uint8_t* tile = bexp + (int64_t)w * npad * 32;
+            for (int j0 = 0; j0 < a; j0 += 16) {
+                const int j = j0 + (lane >> 1), half = lane & 1;
+                const uint32_t p = __shfl_sync(0xffffffffu, mine, j & 31);
+                if (j < a) {
+                    uint4 v;
+                    uint32_t* vv = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        const int r = 4 * half + t;
+                        vv[t] = ((p >> r) & 0x01010101u) << (7 - r);
+                    }
+                    const int n = b * a + j;
+                    *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + half * 128 + (n & 7) * 16) = v;
+                }
+            }
+            if (b == (int)gridDim.y - 1) {   // zero padding rows n in [a*B, npad)
+                const int n = (int)gridDim.y * a + (lane >> 1), half = lane & 1;
+                if (n < npad)
+                    *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + half * 128 + (n & 7) * 16) =
+                        make_uint4(0u, 0u, 0u, 0u);
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
@@ -104,10 +145,9 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
 }  // namespace
 
 cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kwords, int a,
-                             int act_frac, void* ws, cudaStream_t s)
+                             int act_frac, void* ws, const WsLayout& l, cudaStream_t s)
 {
     if (B == 0 || kwords == 0) return cudaSuccess;
-    const WsLayout l = ws_layout(B, kwords, a);
     char* base = static_cast<char*>(ws);
     const int nsplit = act_nsplit(kwords);
     const int wpc = (int)((kwords + nsplit - 1) / nsplit);
@@ -124,7 +164,8 @@ cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kword
     return cudaLaunchKernelEx(&cfg, act_quant_transpose_kernel, x, K, kwords, a, act_frac, wpc,
                               reinterpret_cast<int32_t*>(base + l.off_f),
                               reinterpret_cast<long long*>(base + l.off_xsum),
-                              reinterpret_cast<uint32_t*>(base + l.off_planes));
+                              reinterpret_cast<uint32_t*>(base + l.off_planes),
+                              reinterpret_cast<uint8_t*>(base + l.off_bexp), l.npad);
 }
 
 }  // namespace pb

@@ -386,7 +386,8 @@ pb_status pb_act_quantize(const float* x, int64_t batch, int64_t cols, int32_t a
     if (st != PB_OK) return st;
     if ((st = check_ws(ws, ws_bytes, batch, cols, act_bits)) != PB_OK) return st;
     if (batch * cols > 0 && (!x || !aligned(x, 4))) return fail(PB_EINVAL, "x must be a non-NULL device pointer");
-    cudaError_t e = pb::launch_act_quant(x, batch, cols, pb_kwords(cols), act_bits, act_frac, ws,
+    const pb::WsLayout l = pb::ws_layout(batch, pb_kwords(cols), act_bits);
+    cudaError_t e = pb::launch_act_quant(x, batch, cols, pb_kwords(cols), act_bits, act_frac, ws, l,
                                          static_cast<cudaStream_t>(s));
     if (e != cudaSuccess) return cuda_fail(e, "act_quant_transpose launch");
     return PB_OK;
@@ -418,7 +419,7 @@ pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_we
     if (batch == 0 || w->rows == 0) return PB_OK;
 
     const pb::WsLayout l = pb::ws_layout(batch, w->kwords, act_bits);
-    const char* base = static_cast<const char*>(ws);
+    char* base = static_cast<char*>(const_cast<void*>(ws));
     pb::GemmArgs g;
     g.bits = w->bits;
     g.R = w->rows;
@@ -438,14 +439,19 @@ pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_we
     g.bias = bias;
     g.fn = fn;
     g.accumulate = accumulate ? 1 : 0;
+    g.npad = l.npad;
+    g.bexp = reinterpret_cast<const uint8_t*>(base + l.off_bexp);
+    g.slots = reinterpret_cast<unsigned long long*>(base + l.off_slots);
+    g.counters = reinterpret_cast<int*>(base + l.off_count);
 
     cudaError_t e;
     const cudaStream_t cs = static_cast<cudaStream_t>(s);
     if (g_engine == PB_ENGINE_MMA) {
-        if (!pb::mma_supported(g)) return fail(PB_EINVAL, "PB_ENGINE_MMA does not support this shape");
-        e = pb::launch_gemm_mma(g, cs);
-    } else if (g_engine == PB_ENGINE_AUTO && pb::mma_supported(g)) {
-        e = pb::launch_gemm_mma(g, cs);
+        if (!pb::tc_supported(g))
+            return fail(PB_EINVAL, "PB_ENGINE_MMA needs act_bits*batch <= 32 and k_used*N_pad <= 256");
+        e = pb::launch_gemm_tc(g, cs);
+    } else if (g_engine == PB_ENGINE_AUTO && pb::tc_supported(g)) {
+        e = pb::launch_gemm_tc(g, cs);
     } else {
         e = pb::launch_gemv_popc(g, cs);
     }

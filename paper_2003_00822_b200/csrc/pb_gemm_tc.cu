@@ -1,0 +1,507 @@
+// pb_gemm_tc.cu -- steps a3-a5 on the 5th-generation tensor cores (engine MMA).
+//
+// The 0/1 products of P:205-206 (W_i[r,c] AND X_j[b,c], summed over c) are
+// computed by tcgen05.mma.kind::i8 (u8 x u8 -> s32, SASS UTCIMMA) with both
+// operands holding single bits:
+//   A (TMEM, M = 128 rows x K = 32 bytes): one packed weight word w (32
+//     columns of one bitlayer row) becomes 8 registers A_r = w & (0x01010101 << r),
+//     r = 0..7: byte q of A_r is 2^r * bit(8q + r) -- one LOP3 per 4 columns,
+//     stored with tcgen05.st.32x32b (lane = row, TMEM column r = bytes k = 4r..4r+3);
+//   B (SMEM, N_pad plane rows x 32 bytes): byte k = 4r + q of plane row n is
+//     2^(7-r) * X_n bit(8q + r) (written by the activation kernel, pb_act.cu);
+// so every product is 128 * (w_bit AND x_bit) and D[row][n] = 128 * C_in exactly
+// (int32, K < 2^24).  Sign handling, plane weights T_j and layer weights S_i
+// are applied in the exact int64 epilogue, as in the POPC engine.
+//
+// Work decomposition: stream-K over units (128-row tile, 32-word K-chunk);
+// each CTA (one per SM, persistent) walks a contiguous unit range.  For a row
+// tile every layer i < k_used has its own TMEM accumulator (k_used * N_pad
+// columns), so each B chunk staged in SMEM serves all layers.  A CTA that
+// covers a whole tile writes y directly; a CTA holding part of a tile parks
+// its int64 sums in its own slot and bumps the tile's arrival counter; the
+// last arriving CTA sums the slots of all contributors (fixed order, exact)
+// and resets the counter, so the workspace is left as it was found.
+//
+// Warp roles (11 warps):
+//   warp 0      weight producer: TMA (cp.async.bulk.tensor.3d, 128B swizzle)
+//               of 128-row x 32-word bitlayer tiles into a 6-stage SMEM ring;
+//               starts before the activation kernel finishes (PDL);
+//   warp 1      TMEM allocator and single-thread MMA issuer;
+//   warp 2      B producer: 1-D bulk copies of the plane tiles (after PDL wait);
+//   warps 3..10 converters: thread = weight row; read the row's words from
+//               the swizzled SMEM tile, build A tiles, tcgen05.st them into an
+//               8-slot TMEM ring; warps 3..6 also run the epilogue.
+#include <cuda.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "pb_common.cuh"
+#include "pb_internal.h"
+
+namespace pb {
+namespace {
+
+constexpr int kConvWarps = 8;
+constexpr int kConv0 = 3;                     // first converter warp
+constexpr int kThreads = 32 * (kConv0 + kConvWarps);
+constexpr int kSlots = 8;                     // A ring: 8 slots x 32 TMEM columns (4 A tiles each)
+constexpr int kGroup = 4;                     // words per converter step (= A tiles per slot)
+constexpr int kChunkWords = 32;               // K-chunk = one 128-byte swizzle row
+constexpr int kWStages = 6;                   // weight tile ring
+constexpr uint32_t kWTileBytes = kTcRows * kChunkWords * 4;   // 16 KiB
+constexpr int kDCol = 256;                    // D accumulators start at TMEM column 256
+constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * kChunkWords * 32 * 32;
+
+struct Bars {
+    uint64_t a_full[kSlots], a_empty[kSlots];
+    uint64_t w_full[kWStages], w_empty[kWStages];
+    uint64_t b_full[2], b_empty[2];
+    uint64_t d_full, d_empty;
+    uint32_t tmem_base;
+    int last_flag;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// K-major, no swizzle: core matrix = 8 rows x 16 B; LBO = 128 B (K-adjacent),
+// SBO = 256 B (next 8 rows); version 1 (sm_100).
+__device__ __forceinline__ uint64_t b_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+           ((uint64_t)1 << 46);
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void st_tmem_x32(uint32_t addr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(addr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void ld_tmem_x8(uint32_t addr, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(addr)
+                 : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Host-chosen decomposition.
+struct TcPlan {
+    int tiles;        // ceil(R / 128)
+    int chunks;       // 32-word K-chunks per tile
+    long long units;  // tiles * chunks
+};
+
+__device__ __forceinline__ int chunk_groups(const GemmArgs& g, int kc) {
+    int64_t n = g.kwords - (int64_t)kc * kChunkWords;
+    if (n > kChunkWords) n = kChunkWords;
+    return (int)(n / kGroup);
+}
+
+// A CTA's units [u0, u1) split into segments of one row tile: [kcA, kcB) of tile rt.
+struct Seg {
+    int rt, kcA, kcB;
+    long long next;
+};
+__device__ __forceinline__ Seg segment(const TcPlan& p, long long u, long long u1) {
+    Seg s;
+    s.rt = (int)(u / p.chunks);
+    s.kcA = (int)(u - (long long)s.rt * p.chunks);
+    long long ue = (long long)(s.rt + 1) * p.chunks;
+    if (ue > u1) ue = u1;
+    s.kcB = s.kcA + (int)(ue - u);
+    s.next = ue;
+    return s;
+}
+
+template <int NPAD>
+__global__ void __launch_bounds__(kThreads, 1)
+bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUtensorMap wmap)
+{
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment for the 128B-swizzled TMA tiles
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Bars& bars = *reinterpret_cast<Bars*>(smem);
+    uint8_t* wtile0 = smem + 1024;
+    uint8_t* btile0 = wtile0 + kWStages * kWTileBytes;
+    constexpr uint32_t kBStage = kChunkWords * NPAD * 32;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long G = gridDim.x;
+    const long long u0 = p.units * blockIdx.x / G, u1 = p.units * (blockIdx.x + 1) / G;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSlots; ++s) {
+            mbar_init(&bars.a_full[s], 4);
+            mbar_init(&bars.a_empty[s], 1);
+        }
+        for (int s = 0; s < kWStages; ++s) {
+            mbar_init(&bars.w_full[s], 1);
+            mbar_init(&bars.w_empty[s], kConvWarps);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&bars.b_full[s], 1);
+            mbar_init(&bars.b_empty[s], 1);
+        }
+        mbar_init(&bars.d_full, 1);
+        mbar_init(&bars.d_empty, 4);
+        fence_mbar_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(&bars.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bars.tmem_base;
+    pdl_trigger();
+
+    if (warp == 0) {
+        // ------------------------------------------------ weight tile producer (no PDL wait:
+        // the packed weights do not depend on the activation kernel).  Whole warp walks the
+        // schedule, one elected lane issues.
+        int tc = 0;
+        for (long long u = u0; u < u1;) {
+            const Seg sg = segment(p, u, u1);
+            for (int kc = sg.kcA; kc < sg.kcB; ++kc)
+                for (int i = 0; i < g.k_used; ++i, ++tc) {
+                    const int st = tc % kWStages;
+                    mbar_wait(&bars.w_empty[st], (uint32_t)(((tc / kWStages) & 1) ^ 1));
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&bars.w_full[st], kWTileBytes);
+                        tma_load_3d(wtile0 + st * kWTileBytes, &wmap, kc * kChunkWords, sg.rt * kTcRows, i,
+                                    &bars.w_full[st]);
+                    }
+                    __syncwarp();
+                }
+            u = sg.next;
+        }
+    } else if (warp == 2) {
+        // ------------------------------------------------ B (plane tile) producer
+        pdl_wait();
+        int cc = 0;
+        for (long long u = u0; u < u1;) {
+            const Seg sg = segment(p, u, u1);
+            for (int kc = sg.kcA; kc < sg.kcB; ++kc, ++cc) {
+                const int st = cc & 1;
+                mbar_wait(&bars.b_empty[st], (uint32_t)(((cc >> 1) & 1) ^ 1));
+                if (elect_one()) {
+                    const uint32_t bytes = (uint32_t)chunk_groups(g, kc) * kGroup * NPAD * 32;
+                    mbar_arrive_expect_tx(&bars.b_full[st], bytes);
+                    bulk_g2s(btile0 + st * kBStage, g.bexp + (int64_t)kc * kChunkWords * NPAD * 32, bytes,
+                             &bars.b_full[st]);
+                }
+                __syncwarp();
+            }
+            u = sg.next;
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer: the whole warp walks the
+        // schedule (warp-uniform values stay in uniform registers), one elected lane issues.
+        const uint32_t idesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(NPAD >> 3) << 17) |
+                               ((uint32_t)(kTcRows >> 4) << 24);
+        uint32_t gidx = 0;
+        int cc = 0, seg = 0;
+        for (long long u = u0; u < u1; ++seg) {
+            const Seg sg = segment(p, u, u1);
+            if (seg > 0) mbar_wait(&bars.d_empty, (uint32_t)((seg - 1) & 1));
+            tc_fence_after();
+            for (int kc = sg.kcA; kc < sg.kcB; ++kc, ++cc) {
+                const int st = cc & 1;
+                mbar_wait(&bars.b_full[st], (uint32_t)((cc >> 1) & 1));
+                tc_fence_after();
+                const uint64_t bdesc0 = b_desc(smem_u32(btile0 + st * kBStage));
+                const int ng = chunk_groups(g, kc);
+                for (int i = 0; i < g.k_used; ++i) {
+                    const uint32_t dcol = tmem + kDCol + (uint32_t)(i * NPAD);
+                    for (int grp = 0; grp < ng; ++grp, ++gidx) {
+                        const uint32_t slot = gidx % kSlots;
+                        mbar_wait(&bars.a_full[slot], (gidx / kSlots) & 1);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            // descriptor start address advances 16 B units: one B tile = NPAD*32 B
+                            uint64_t bd = bdesc0 + (uint64_t)(grp * kGroup * (NPAD * 32 / 16));
+                            const uint32_t a0 = tmem + slot * 32;
+                            const uint32_t acc0 = (kc == sg.kcA && grp == 0) ? 0u : 1u;
+                            tc_mma(dcol, a0, bd, idesc, acc0);
+                            tc_mma(dcol, a0 + 8, bd + (NPAD * 32 / 16), idesc, 1u);
+                            tc_mma(dcol, a0 + 16, bd + 2 * (NPAD * 32 / 16), idesc, 1u);
+                            tc_mma(dcol, a0 + 24, bd + 3 * (NPAD * 32 / 16), idesc, 1u);
+                            tc_commit(&bars.a_empty[slot]);
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (elect_one()) tc_commit(&bars.b_empty[st]);
+                __syncwarp();
+            }
+            if (elect_one()) tc_commit(&bars.d_full);
+            __syncwarp();
+            u = sg.next;
+        }
+    } else {
+        // ------------------------------------------------ converters (+ epilogue)
+        const int cw = warp - kConv0;
+        const int h = cw >> 2;                 // 0: warps 3..6, 1: warps 7..10
+        const int q = warp & 3;                // TMEM lane quarter this warp may access
+        const int m = q * 32 + lane;           // row within the tile
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        long long gidx = 0;
+        int tc = 0, seg = 0;
+        for (long long u = u0; u < u1; ++seg) {
+            const Seg sg = segment(p, u, u1);
+            const int64_t row = (int64_t)sg.rt * kTcRows + m;
+            const bool row_ok = row < g.R;
+            for (int kc = sg.kcA; kc < sg.kcB; ++kc) {
+                const int ng = chunk_groups(g, kc);
+                for (int i = 0; i < g.k_used; ++i, ++tc) {
+                    const int st = tc % kWStages;
+                    mbar_wait(&bars.w_full[st], (uint32_t)((tc / kWStages) & 1));
+                    const uint8_t* trow = wtile0 + st * kWTileBytes + m * 128;
+                    for (int grp = (int)((h - (gidx & 1)) & 1); grp < ng; grp += 2) {
+                        const long long gi = gidx + grp;
+                        // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
+                        const uint4 w = *reinterpret_cast<const uint4*>(trow + ((grp ^ (m & 7)) << 4));
+                        const int slot = (int)(gi % kSlots);
+                        mbar_wait(&bars.a_empty[slot], (uint32_t)(((gi / kSlots) & 1) ^ 1));
+                        tc_fence_after();
+                        uint32_t v[32];
+                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int uu = 0; uu < 4; ++uu)
+#pragma unroll
+                            for (int r = 0; r < 8; ++r) v[uu * 8 + r] = ws[uu] & (0x01010101u << r);
+                        st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 32), v);
+                        tmem_st_wait();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&bars.a_full[slot]);
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&bars.w_empty[st]);
+                    gidx += ng;
+                }
+            }
+
+            if (h == 0) {
+                // ---------------- epilogue: fold D (k_used x NPAD) into exact int64
+                mbar_wait(&bars.d_full, (uint32_t)(seg & 1));
+                tc_fence_after();
+                pdl_wait();
+                // cs[n] = sum_i S_i * C_in  (D holds 128 * C_in)
+                unsigned long long cs[NPAD];
+#pragma unroll
+                for (int n = 0; n < NPAD; ++n) cs[n] = 0;
+                for (int i = 0; i < g.k_used; ++i) {
+                    uint32_t dv[NPAD];
+#pragma unroll
+                    for (int c = 0; c < NPAD; c += 8) {
+                        uint32_t t8[8];
+                        ld_tmem_x8(tmem + lane_off + kDCol + (uint32_t)(i * NPAD + c), t8);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) dv[c + e] = t8[e];
+                    }
+                    tmem_ld_wait();
+                    const unsigned long long Si = layer_scale(g.L, g.offset, i);
+#pragma unroll
+                    for (int n = 0; n < NPAD; ++n) cs[n] += Si * (unsigned long long)(dv[n] >> 7);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars.d_empty);
+                // tot_b = sum_j T_j cs[b*a + j]
+                auto tot_of = [&](int b) -> unsigned long long {
+                    unsigned long long t = 0;
+#pragma unroll
+                    for (int n = 0; n < NPAD; ++n) {
+                        const int j = n - b * g.a;
+                        if (j >= 0 && j < g.a) t += plane_scale(g.a, j) * cs[n];
+                    }
+                    return t;
+                };
+                const bool whole = (sg.kcA == 0 && sg.kcB == p.chunks);
+                bool finalize = whole;
+                if (!whole) {
+                    // partial tile: park this CTA's sums in its slot (first segment of
+                    // the range -> slot 0, otherwise it is the last -> slot 1)
+                    const int myslot = (u == u0) ? 0 : 1;
+                    unsigned long long* sl = g.slots + (((int64_t)blockIdx.x * 2 + myslot) * g.B) * kTcRows;
+                    for (int b = 0; b < g.B; ++b) sl[b * kTcRows + m] = tot_of(b);
+                    __threadfence();
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (cw == 0 && lane == 0) {
+                        const int add = sg.kcB - sg.kcA;
+                        const int old = atomicAdd(&g.counters[sg.rt], add);
+                        const int last = (old + add == p.chunks);
+                        if (last) g.counters[sg.rt] = 0;      // every call leaves the counters zero
+                        bars.last_flag = last;
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    finalize = bars.last_flag != 0;
+                    if (finalize) __threadfence();
+                }
+                if (finalize && row_ok) {
+                    for (int b = 0; b < g.B; ++b) {
+                        unsigned long long t;
+                        if (whole) {
+                            t = tot_of(b);
+                        } else {
+                            // sum the slots of every CTA whose unit range meets this tile
+                            t = 0;
+                            const long long t0u = (long long)sg.rt * p.chunks, t1u = t0u + p.chunks;
+                            long long c = (t0u * G) / p.units;
+                            while (c > 0 && p.units * c / G > t0u) --c;
+                            while (p.units * (c + 1) / G <= t0u) ++c;
+                            for (; c < G && p.units * c / G < t1u; ++c) {
+                                const long long cu0 = p.units * c / G, cu1 = p.units * (c + 1) / G;
+                                if (cu1 <= cu0) continue;
+                                const int sslot = (cu0 >= t0u) ? 0 : 1;
+                                t += __ldcg(g.slots + (((int64_t)c * 2 + sslot) * g.B + b) * kTcRows + m);
+                            }
+                        }
+                        if (g.offset) {
+                            unsigned long long sx = 0;
+                            for (int pp = 0; pp < g.nsplit; ++pp)
+                                sx += (unsigned long long)g.xsum[(int64_t)b * kMaxSplit + pp];
+                            t += (unsigned long long)g.offset * sx;
+                        }
+                        const long long accv = (long long)t;
+                        const int64_t o = (int64_t)b * g.R + row;
+                        if (g.acc) g.acc[o] = accv;
+                        float yv = dequant(accv, g.scale, g.f[b]);
+                        if (g.bias) yv += g.bias[row];
+                        if (g.accumulate) yv += g.y[o];
+                        g.y[o] = apply_fn(yv, g.fn);
+                    }
+                }
+            }
+            u = sg.next;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+cudaError_t make_weight_map(const GemmArgs& g, CUtensorMap* map)
+{
+    static EncodeTiledFn encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+        encode = reinterpret_cast<EncodeTiledFn>(fn);
+    }
+    // bits[L][R][kwords] uint32 as a 3-D tensor {kwords, R, L}; box {32 words, 128 rows, 1}.
+    // Out-of-range rows / words (tile tails) are filled with zeros by the TMA unit.
+    const cuuint64_t dims[3] = {(cuuint64_t)g.kwords, (cuuint64_t)g.R, (cuuint64_t)g.L};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.kwords * 4, (cuuint64_t)g.kwords * 4 * (cuuint64_t)g.R};
+    const cuuint32_t box[3] = {kChunkWords, kTcRows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(g.bits), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int NPAD>
+cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
+{
+    static int sms = 0;
+    static bool attr = false;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)kSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    CUtensorMap map;
+    cudaError_t e = make_weight_map(g, &map);
+    if (e != cudaSuccess) return e;
+    TcPlan p;
+    p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
+    p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
+    p.units = (long long)p.tiles * p.chunks;
+    long long grid = p.units < sms ? p.units : sms;
+    if (grid > kMaxCtas) grid = kMaxCtas;
+
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.stream = s;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, bitgemm_tc_kernel<NPAD>, g, p, map);
+}
+
+}  // namespace
+
+bool tc_supported(const GemmArgs& g)
+{
+    return g.npad > 0 && g.k_used * g.npad <= 256 && g.kwords > 0 && g.R > 0 && g.B > 0 &&
+           (g.R + kTcRows - 1) / kTcRows <= kMaxTiles && g.L <= 16;
+}
+
+cudaError_t launch_gemm_tc(const GemmArgs& g, cudaStream_t s)
+{
+    switch (g.npad) {
+        case 8: return launch_t<8>(g, s);
+        case 16: return launch_t<16>(g, s);
+        case 32: return launch_t<32>(g, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace pb

@@ -1,5 +1,5 @@
 // pb_internal.h -- launchers shared between the host API (pb_api.cpp) and the
-// sm_100a kernels (pb_act.cu, pb_gemv_popc.cu, pb_gemm_mma.cu, pb_cells.cu).
+// sm_100a kernels (pb_act.cu, pb_gemv_popc.cu, pb_gemm_tc.cu, pb_cells.cu).
 // Product code only; nothing here is shared with oracle/.
 #pragma once
 #include <cstddef>
@@ -10,19 +10,44 @@ namespace pb {
 
 constexpr int kMaxSplit = 64;        // activation kernel CTAs per batch column (max)
 constexpr size_t kAlign = 256;
+constexpr int kTcRows = 128;         // tensor engine row tile (MMA M)
+constexpr int kTcMaxN = 32;          // tensor engine: a * batch <= 32 (MMA N padded to 8/16/32)
 
 inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
 
-// Workspace carve-up (documented in pb.h, pb_workspace_bytes).
+// MMA N (plane columns a*batch padded to a legal tcgen05 kind::i8 N for M = 128),
+// 0 when the tensor engine's operand tiles are not produced for this shape.
+inline int tc_npad(int64_t batch, int32_t a) {
+    const int64_t n = batch * a;
+    if (n <= 0 || n > kTcMaxN) return 0;
+    return n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+}
+
+// Workspace carve-up (documented in pb.h, pb_workspace_bytes):
+//   [tile counters int32 x kMaxTiles]   stream-K arrival counters; zero on
+//                                       entry, every call leaves them zero
+//   [partial slots int64 x kMaxCtas x 2 x B x 128]   tensor engine only
+//   [f_b int32 x B][Σx_q partials int64 x B x 64][bit planes [B][a][kwords]]
+//   [tensor-engine B operand tiles: kwords x N_pad x 32 bytes]
+// Every region except the counters is fully rewritten by each call, so one
+// zero-filled workspace can serve calls of any shape (not concurrently).
+constexpr int kMaxTiles = 8192;      // tensor engine: rows <= 8192 * 128
+constexpr int kMaxCtas = 160;        // tensor engine grid cap (B200: 148 SMs)
 struct WsLayout {
-    size_t off_f, off_xsum, off_planes, total;
+    size_t off_count, off_slots, off_f, off_xsum, off_planes, off_bexp, total;
+    int npad;
 };
 inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     WsLayout l;
-    l.off_f = 0;
-    l.off_xsum = align_up(sizeof(int32_t) * (size_t)batch);
+    l.npad = tc_npad(batch, act_bits);
+    l.off_count = 0;
+    l.off_slots = align_up(sizeof(int32_t) * kMaxTiles);
+    const size_t slots = l.npad ? sizeof(long long) * kMaxCtas * 2 * (size_t)batch * kTcRows : 0;
+    l.off_f = align_up(l.off_slots + slots);
+    l.off_xsum = align_up(l.off_f + sizeof(int32_t) * (size_t)batch);
     l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kMaxSplit);
-    l.total = align_up(l.off_planes + sizeof(uint32_t) * (size_t)batch * act_bits * kwords);
+    l.off_bexp = align_up(l.off_planes + sizeof(uint32_t) * (size_t)batch * act_bits * kwords);
+    l.total = align_up(l.off_bexp + (size_t)kwords * 32 * (size_t)l.npad);
     return l;
 }
 
@@ -48,13 +73,18 @@ struct GemmArgs {
     const float* bias;      // [R] or null
     int fn;
     int accumulate;
+    // tensor engine operands (valid when npad > 0)
+    int npad;
+    const uint8_t* bexp;          // [kwords][npad x 32 canonical tile]
+    unsigned long long* slots;    // [kMaxCtas][2][B][128] partial tile sums
+    int* counters;                // [kMaxTiles]
 };
 
 cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kwords, int a,
-                             int act_frac, void* ws, cudaStream_t s);
+                             int act_frac, void* ws, const WsLayout& l, cudaStream_t s);
 cudaError_t launch_gemv_popc(const GemmArgs& g, cudaStream_t s);
-cudaError_t launch_gemm_mma(const GemmArgs& g, cudaStream_t s);
-bool mma_supported(const GemmArgs& g);
+cudaError_t launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
+bool tc_supported(const GemmArgs& g);
 cudaError_t launch_lstm_cell(const float* gates, const float* c, int64_t B, int64_t H,
                              float* h_out, float* c_out, cudaStream_t s);
 cudaError_t launch_rnn_cell(const float* gates, int64_t B, int64_t H, float* h_out,

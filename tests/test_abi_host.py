@@ -124,10 +124,11 @@ def test_memory_model(pb):
 def test_validation_before_launch(pb):
     # every argument error is reported before any CUDA call (no device here)
     d = pb.pb_weights(16, 8, 64, 4, 4, 0, 1.0)
-    ws = np.zeros(4096, np.uint8)
+    ws = np.zeros(400000 + 256, np.uint8)
+    assert pb.pb_workspace_bytes(1, 64, 16) <= 400000
     wsp = (ws.ctypes.data + 255) // 256 * 256
     y = np.zeros(64, np.float32)
-    args = lambda k, a, frac=pb.PB_ACT_AUTO: (16, 1, C.byref(d), k, a, frac, y.ctypes.data, None, wsp, 2048, None)
+    args = lambda k, a, frac=pb.PB_ACT_AUTO: (16, 1, C.byref(d), k, a, frac, y.ctypes.data, None, wsp, 400000, None)
     assert pb.pb_matmul(*args(0, 16)) == pb.PB_EINVAL
     assert pb.pb_matmul(*args(5, 16)) == pb.PB_EINVAL
     assert b"k_used" in pb.pb_last_error()
@@ -143,10 +144,10 @@ def test_validation_before_launch(pb):
     assert pb.pb_matmul(16, 1, C.byref(big), 16, 32, pb.PB_ACT_AUTO, y.ctypes.data, None, wbp,
                         pb.pb_workspace_bytes(1, 1 << 17, 32), None) == pb.PB_ERANGE
     bad_off = pb.pb_weights(16, 8, 64, 4, 4, 1, 1.0)
-    assert pb.pb_matmul(16, 1, C.byref(bad_off), 1, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, 2048,
+    assert pb.pb_matmul(16, 1, C.byref(bad_off), 1, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, 400000,
                         None) == pb.PB_EINVAL
     mis = pb.pb_weights(20, 8, 64, 4, 4, 0, 1.0)   # misaligned bits
-    assert pb.pb_matmul(*(16, 1, C.byref(mis), 4, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, 2048,
+    assert pb.pb_matmul(*(16, 1, C.byref(mis), 4, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, 400000,
                           None)) == pb.PB_EINVAL
     assert pb.pb_set_engine(7) == pb.PB_EINVAL
 
@@ -163,7 +164,7 @@ def test_shard_rows_partition(pb, R, N):
 
 
 def test_workspace_layout(pb):
-    assert pb.pb_workspace_bytes(1, 16384, 16) >= 16 * 16384 // 8
+    assert pb.pb_workspace_bytes(1, 16384, 16) >= 16 * 16384 // 8 + 16 * 16384
     assert pb.pb_workspace_bytes(128, 4096, 16) >= 128 * 16 * 4096 // 8
     assert pb.pb_workspace_bytes(1, 10, 0) == 0
     assert pb.pb_rowshard_workspace_bytes(4, 1024, 16, 1000, 8) >= pb.pb_workspace_bytes(4, 1024, 16) + 4 * 4 * 125 * 9

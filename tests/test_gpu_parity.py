@@ -193,3 +193,26 @@ def test_latency_drops_with_fewer_layers(pb, torch):
         torch.cuda.synchronize()
         times[k] = e0.elapsed_time(e1) / 20
     assert times[16] > times[8] > times[4] > times[1], times
+
+
+@pytest.mark.parametrize("R,K,B,L,k_used,a", [(1024, 8192, 1, 4, 4, 16), (1000, 3000, 2, 8, 5, 16),
+                                              (300, 4096, 4, 3, 3, 8), (129, 1000, 1, 16, 16, 16),
+                                              (2048, 2048, 1, 8, 8, 32), (640, 6000, 3, 2, 2, 5)])
+def test_tc_streamk_repeat(pb, torch, orc, R, K, B, L, k_used, a):
+    # tensor engine: stream-K partial tiles + self-cleaning scratch across calls
+    s = synth.seed(2, 3000 + R + K)
+    m = synth.codes(R, K, L, s)
+    x = synth.inject_edges(synth.activations(B, K, s + 1, "gauss"), s + 2)
+    w = pb.PackedWeights.from_codes(m, L, 0, 0.5)
+    ws = pb.Workspace(pb.workspace_bytes(B, K, a))
+    xd = torch.from_numpy(x).cuda()
+    acc_o, y_o, _ = orc.pbatch(m, L, 0, 0.5, k_used, x, a, nthreads=8)
+    pb.set_engine(pb.PB_ENGINE_MMA)
+    try:
+        for rep in range(3):
+            acc = torch.zeros((B, R), dtype=torch.int64, device="cuda")
+            y = pb.matmul(xd, w, k_used, a, acc=acc, ws=ws)
+            torch.cuda.synchronize()
+            compare(acc.cpu().numpy(), y.cpu().numpy(), acc_o, y_o)
+    finally:
+        pb.set_engine(pb.PB_ENGINE_AUTO)
