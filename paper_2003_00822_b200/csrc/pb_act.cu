@@ -5,11 +5,13 @@
 // One warp turns 32 consecutive columns into `a` plane words with `a`
 // __ballot_sync votes (VOTE.ANY), sign plane first.  Σ_c x_q (needed only for
 // the binary-mode offset term) is produced as per-CTA partial sums.
-// When the tensor engine is used (a*B <= 32) the kernel also emits, per
-// 32-column k-block, the MMA B operand tile (N_pad plane rows x 32 bytes,
-// K-major no-swizzle canonical layout): byte kk = 4r + q of plane row n holds
-// bit (8q + r) of that plane word shifted to 2^(7-r), so that against the
-// weight byte 2^r * w_bit (pb_gemm_tc.cu) every 0/1 product is exactly 128.
+// When the tensor engine is used (a*B <= 32) the kernel also emits the MMA
+// B operand (tcgen05 kind::mxf4, packed e2m1, K-major no-swizzle canonical
+// layout): per 2 words (64 columns) one N_pad x 32-byte tile.  The 16 bytes
+// of word w in plane row n are 4 uint32 (r = 0..3) whose nibble e holds
+// X_n bit (4e + r) times the e2m1 code {2.0, 1.0, 0.5, 0.5}[r]; against the
+// weight nibbles {0.5, 1.0, 2.0, 2.0}[r] * w_bit (pb_gemm_tc.cu) every 0/1
+// product is exactly 1.0.
 //
 // Grid: (nsplit, B) CTAs of 512 threads.  Every CTA recomputes max|x[b,:]|
 // (an L2-resident re-read of K floats) so no second launch or grid sync is
@@ -105,29 +107,18 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
         }
         if (lane < a) pb[(int64_t)lane * kwords + w] = mine;
         if (npad) {
-            // B tile rows n = b*a + j; lane pair (j, half) writes 16 bytes:
-            // uint32 for r = 4*half + t holds bytes q = 0..3 = bit (8q + r) << (7 - r).
-            uint8_t* tile = bexp + (int64_t)w * npad * 32;
-            for (int j0 = 0; j0 < a; j0 += 16) {
-                const int j = j0 + (lane >> 1), half = lane & 1;
-                const uint32_t p = __shfl_sync(0xffffffffu, mine, j & 31);
-                if (j < a) {
-                    uint4 v;
-                    uint32_t* vv = reinterpret_cast<uint32_t*>(&v);
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int r = 4 * half + t;
-                        vv[t] = ((p >> r) & 0x01010101u) << (7 - r);
-                    }
-                    const int n = b * a + j;
-                    *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + half * 128 + (n & 7) * 16) = v;
-                }
-            }
+            // tile (w / 2), k-half (w % 2); lane j < a writes plane row n = b*a + j
+            uint8_t* tile = bexp + (int64_t)(w >> 1) * npad * 32 + (w & 1) * 128;
+            const uint32_t p = mine;
+            auto put = [&](int n, uint4 v) {
+                *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + (n & 7) * 16) = v;
+            };
+            if (lane < a)
+                put(b * a + lane, make_uint4(((p >> 0) & 0x11111111u) * 4u, ((p >> 1) & 0x11111111u) * 2u,
+                                             (p >> 2) & 0x11111111u, (p >> 3) & 0x11111111u));
             if (b == (int)gridDim.y - 1) {   // zero padding rows n in [a*B, npad)
-                const int n = (int)gridDim.y * a + (lane >> 1), half = lane & 1;
-                if (n < npad)
-                    *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + half * 128 + (n & 7) * 16) =
-                        make_uint4(0u, 0u, 0u, 0u);
+                const int n = (int)gridDim.y * a + lane;
+                if (n < npad) put(n, make_uint4(0u, 0u, 0u, 0u));
             }
         }
     }

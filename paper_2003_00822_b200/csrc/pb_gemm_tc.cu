@@ -1,17 +1,23 @@
 // pb_gemm_tc.cu -- steps a3-a5 on the 5th-generation tensor cores (engine MMA).
 //
 // The 0/1 products of P:205-206 (W_i[r,c] AND X_j[b,c], summed over c) are
-// computed by tcgen05.mma.kind::i8 (u8 x u8 -> s32, SASS UTCIMMA) with both
-// operands holding single bits:
-//   A (TMEM, M = 128 rows x K = 32 bytes): one packed weight word w (32
-//     columns of one bitlayer row) becomes 8 registers A_r = w & (0x01010101 << r),
-//     r = 0..7: byte q of A_r is 2^r * bit(8q + r) -- one LOP3 per 4 columns,
-//     stored with tcgen05.st.32x32b (lane = row, TMEM column r = bytes k = 4r..4r+3);
-//   B (SMEM, N_pad plane rows x 32 bytes): byte k = 4r + q of plane row n is
-//     2^(7-r) * X_n bit(8q + r) (written by the activation kernel, pb_act.cu);
-// so every product is 128 * (w_bit AND x_bit) and D[row][n] = 128 * C_in exactly
-// (int32, K < 2^24).  Sign handling, plane weights T_j and layer weights S_i
-// are applied in the exact int64 epilogue, as in the POPC engine.
+// computed by tcgen05.mma.kind::mxf4.block_scale (packed e2m1 x e2m1 -> f32,
+// SASS UTCOMMA, all E8M0 block scales = 1.0) with both operands holding
+// single bits:
+//   A (TMEM, M = 128 rows x K = 64 e2m1 = 32 bytes): one packed weight word
+//     w (32 columns of one bitlayer row) becomes 4 registers of 8 nibbles,
+//       w & 0x11111111 (0.5), w & 0x22222222 (1.0), w & 0x44444444 (2.0),
+//       (w >> 1) & 0x44444444 (2.0),
+//     so nibble e of register r is bit(4e + r) times {0.5, 1, 2, 2}[r] -- five
+//     ALU ops per 32 columns; stored with tcgen05.st.32x32b (lane = row);
+//   B (SMEM, N_pad plane rows x 32 bytes per 64 columns): the same nibble
+//     positions hold plane bits times {2, 1, 0.5, 0.5}[r] (pb_act.cu);
+// so every product is exactly 1.0 * (w_bit AND x_bit) and D[row][n] = C_in
+// exactly (f32 sums of ones, K < 2^24).  Sign handling, plane weights T_j and
+// layer weights S_i are applied in the exact int64 epilogue, as in the
+// POPC engine.  (A kind::i8 form with byte operands measured half the rate:
+// on sm_100a an M=128 MMA costs ~55 cycles for any N <= 64, so bits per MMA
+// decide throughput.)
 //
 // Work decomposition: stream-K over units (128-row tile, 32-word K-chunk);
 // each CTA (one per SM, persistent) walks a contiguous unit range.  For a row
@@ -44,13 +50,14 @@ namespace {
 constexpr int kConvWarps = 8;
 constexpr int kConv0 = 3;                     // first converter warp
 constexpr int kThreads = 32 * (kConv0 + kConvWarps);
-constexpr int kSlots = 8;                     // A ring: 8 slots x 32 TMEM columns (4 A tiles each)
-constexpr int kGroup = 4;                     // words per converter step (= A tiles per slot)
+constexpr int kSlots = 7;                     // A ring: 7 slots x 32 TMEM columns (4 A tiles each)
+constexpr int kGroup = 8;                     // words per converter step (= 4 MMAs of K = 64)
+constexpr int kSfCol = 224;                   // block-scale factors (all 1.0): SFA 224.., SFB 232..
 constexpr int kChunkWords = 32;               // K-chunk = one 128-byte swizzle row
 constexpr int kWStages = 6;                   // weight tile ring
 constexpr uint32_t kWTileBytes = kTcRows * kChunkWords * 4;   // 16 KiB
 constexpr int kDCol = 256;                    // D accumulators start at TMEM column 256
-constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * kChunkWords * 32 * 32;
+constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * (kChunkWords / 2) * 32 * 32;
 
 struct Bars {
     uint64_t a_full[kSlots], a_empty[kSlots];
@@ -71,11 +78,12 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                  : "memory");
 }
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                       uint32_t accumulate) {
+                                       uint32_t accumulate, uint32_t sfa, uint32_t sfb) {
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+            d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
         : "memory");
 }
 // K-major, no swizzle: core matrix = 8 rows x 16 B; LBO = 128 B (K-adjacent),
@@ -125,10 +133,12 @@ struct TcPlan {
     long long units;  // tiles * chunks
 };
 
+// groups of 8 words in chunk kc (the last may hold only 4 real words; the TMA
+// zero-fills the rest, so its extra products are 0)
 __device__ __forceinline__ int chunk_groups(const GemmArgs& g, int kc) {
     int64_t n = g.kwords - (int64_t)kc * kChunkWords;
     if (n > kChunkWords) n = kChunkWords;
-    return (int)(n / kGroup);
+    return (int)((n + kGroup - 1) / kGroup);
 }
 
 // A CTA's units [u0, u1) split into segments of one row tile: [kcA, kcB) of tile rt.
@@ -157,7 +167,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     Bars& bars = *reinterpret_cast<Bars*>(smem);
     uint8_t* wtile0 = smem + 1024;
     uint8_t* btile0 = wtile0 + kWStages * kWTileBytes;
-    constexpr uint32_t kBStage = kChunkWords * NPAD * 32;
+    constexpr uint32_t kBTile = NPAD * 32;                    // one MMA's B (64 columns)
+    constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;  // one K-chunk
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long G = gridDim.x;
@@ -190,6 +201,19 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bars.tmem_base;
+    if (warp >= kConv0 && warp < kConv0 + 4) {
+        // E8M0 block scale factors = 1.0 (0x7F) for SFA and SFB, all 128 lanes
+        const uint32_t s7 = 0x7F7F7F7Fu;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                tmem + ((uint32_t)((warp & 3) * 32) << 16) + kSfCol),
+            "r"(s7)
+            : "memory");
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
     pdl_trigger();
 
     if (warp == 0) {
@@ -222,10 +246,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 const int st = cc & 1;
                 mbar_wait(&bars.b_empty[st], (uint32_t)(((cc >> 1) & 1) ^ 1));
                 if (elect_one()) {
-                    const uint32_t bytes = (uint32_t)chunk_groups(g, kc) * kGroup * NPAD * 32;
+                    const uint32_t bytes = (uint32_t)chunk_groups(g, kc) * (kGroup / 2) * kBTile;
                     mbar_arrive_expect_tx(&bars.b_full[st], bytes);
-                    bulk_g2s(btile0 + st * kBStage, g.bexp + (int64_t)kc * kChunkWords * NPAD * 32, bytes,
-                             &bars.b_full[st]);
+                    bulk_g2s(btile0 + st * kBStage, g.bexp + (int64_t)kc * kBStage, bytes, &bars.b_full[st]);
                 }
                 __syncwarp();
             }
@@ -234,8 +257,10 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer: the whole warp walks the
         // schedule (warp-uniform values stay in uniform registers), one elected lane issues.
-        const uint32_t idesc = (2u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(NPAD >> 3) << 17) |
+        // kind::mxf4: A, B = E2M1 (1), scale format UE8M0 (bit 23), K = 64
+        const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(NPAD >> 3) << 17) | (1u << 23) |
                                ((uint32_t)(kTcRows >> 4) << 24);
+        const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 8;
         uint32_t gidx = 0;
         int cc = 0, seg = 0;
         for (long long u = u0; u < u1; ++seg) {
@@ -255,14 +280,14 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         mbar_wait(&bars.a_full[slot], (gidx / kSlots) & 1);
                         tc_fence_after();
                         if (elect_one()) {
-                            // descriptor start address advances 16 B units: one B tile = NPAD*32 B
-                            uint64_t bd = bdesc0 + (uint64_t)(grp * kGroup * (NPAD * 32 / 16));
+                            // descriptor start address advances in 16 B units: one B tile = NPAD*32 B
+                            const uint64_t bd = bdesc0 + (uint64_t)(grp * 4 * (kBTile / 16));
                             const uint32_t a0 = tmem + slot * 32;
                             const uint32_t acc0 = (kc == sg.kcA && grp == 0) ? 0u : 1u;
-                            tc_mma(dcol, a0, bd, idesc, acc0);
-                            tc_mma(dcol, a0 + 8, bd + (NPAD * 32 / 16), idesc, 1u);
-                            tc_mma(dcol, a0 + 16, bd + 2 * (NPAD * 32 / 16), idesc, 1u);
-                            tc_mma(dcol, a0 + 24, bd + 3 * (NPAD * 32 / 16), idesc, 1u);
+                            tc_mma(dcol, a0, bd, idesc, acc0, sfa, sfb);
+                            tc_mma(dcol, a0 + 8, bd + (kBTile / 16), idesc, 1u, sfa, sfb);
+                            tc_mma(dcol, a0 + 16, bd + 2 * (kBTile / 16), idesc, 1u, sfa, sfb);
+                            tc_mma(dcol, a0 + 24, bd + 3 * (kBTile / 16), idesc, 1u, sfa, sfb);
                             tc_commit(&bars.a_empty[slot]);
                         }
                         __syncwarp();
@@ -297,16 +322,20 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     for (int grp = (int)((h - (gidx & 1)) & 1); grp < ng; grp += 2) {
                         const long long gi = gidx + grp;
                         // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
-                        const uint4 w = *reinterpret_cast<const uint4*>(trow + ((grp ^ (m & 7)) << 4));
+                        const uint4 w0 = *reinterpret_cast<const uint4*>(trow + (((2 * grp) ^ (m & 7)) << 4));
+                        const uint4 w1 = *reinterpret_cast<const uint4*>(trow + (((2 * grp + 1) ^ (m & 7)) << 4));
                         const int slot = (int)(gi % kSlots);
                         mbar_wait(&bars.a_empty[slot], (uint32_t)(((gi / kSlots) & 1) ^ 1));
                         tc_fence_after();
                         uint32_t v[32];
-                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+                        const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
-                        for (int uu = 0; uu < 4; ++uu)
-#pragma unroll
-                            for (int r = 0; r < 8; ++r) v[uu * 8 + r] = ws[uu] & (0x01010101u << r);
+                        for (int uu = 0; uu < 8; ++uu) {
+                            v[uu * 4 + 0] = ws[uu] & 0x11111111u;
+                            v[uu * 4 + 1] = ws[uu] & 0x22222222u;
+                            v[uu * 4 + 2] = ws[uu] & 0x44444444u;
+                            v[uu * 4 + 3] = (ws[uu] >> 1) & 0x44444444u;
+                        }
                         st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 32), v);
                         tmem_st_wait();
                         tc_fence_before();
@@ -324,7 +353,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 mbar_wait(&bars.d_full, (uint32_t)(seg & 1));
                 tc_fence_after();
                 pdl_wait();
-                // cs[n] = sum_i S_i * C_in  (D holds 128 * C_in)
+                // cs[n] = sum_i S_i * C_in  (D holds C_in as an exact f32)
                 unsigned long long cs[NPAD];
 #pragma unroll
                 for (int n = 0; n < NPAD; ++n) cs[n] = 0;
@@ -340,7 +369,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     tmem_ld_wait();
                     const unsigned long long Si = layer_scale(g.L, g.offset, i);
 #pragma unroll
-                    for (int n = 0; n < NPAD; ++n) cs[n] += Si * (unsigned long long)(dv[n] >> 7);
+                    for (int n = 0; n < NPAD; ++n) cs[n] += Si * (unsigned long long)__float2uint_rn(__uint_as_float(dv[n]));
                 }
                 tc_fence_before();
                 __syncwarp();

@@ -71,6 +71,54 @@ __global__ void __launch_bounds__(128, 1) mma_rate(long long* out, int iters) {
     if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
 }
 
+template <int N>
+__global__ void __launch_bounds__(128, 1) mma_rate_f4(long long* out, int iters) {
+    __shared__ __align__(1024) uint8_t sB[256 * 32];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t tb;
+    const int w = threadIdx.x >> 5;
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tb)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < 256 * 32; i += 128) sB[i] = (uint8_t)0x22;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t t = tb;
+    const uint32_t s7 = 0x7F7F7F7Fu;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                     t + ((uint32_t)(w * 32) << 16) + 480),
+                 "r"(s7));
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (threadIdx.x == 0) {
+        const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | (8u << 24);
+        const uint64_t bd = desc(smem_u32(sB));
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint32_t acc = i > 0;
+            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+                             t + 256),
+                         "r"(t + (uint32_t)((i & 7) * 8)), "l"(bd), "r"(idesc), "r"(acc), "r"(t + 480), "r"(t + 488));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (blockIdx.x == 0) out[0] = t1 - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
+}
+
 template <bool WAIT>
 __global__ void __launch_bounds__(128, 1) st_rate(long long* out, int iters) {
     __shared__ uint32_t tb;
@@ -214,6 +262,10 @@ void run(const char* name, K k, int iters, double per) {
 
 int main() {
     const int it = 4096;
+    run("mma mxf4 TS M128 N8", mma_rate_f4<8>, it, 1);
+    run("mma mxf4 TS M128 N16", mma_rate_f4<16>, it, 1);
+    run("mma mxf4 TS M128 N32", mma_rate_f4<32>, it, 1);
+    run("mma mxf4 TS M128 N256", mma_rate_f4<256>, it, 1);
     run("mma i8 TS M128 N8", mma_rate<8, true>, it, 1);
     run("mma i8 TS M128 N16", mma_rate<16, true>, it, 1);
     run("mma i8 TS M128 N32", mma_rate<32, true>, it, 1);
