@@ -139,6 +139,14 @@ cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kword
                              int act_frac, void* ws, const WsLayout& l, cudaStream_t s)
 {
     if (B == 0 || kwords == 0) return cudaSuccess;
+    static bool carveout = false;
+    if (!carveout) {
+        // keep the SM in its max-shared-memory configuration between this kernel and
+        // the tensor-engine GEMM (which needs 162 KiB): no L1/SMEM repartition per launch
+        cudaFuncSetAttribute(act_quant_transpose_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+        carveout = true;
+    }
     char* base = static_cast<char*>(ws);
     const int nsplit = act_nsplit(kwords);
     const int wpc = (int)((kwords + nsplit - 1) / nsplit);

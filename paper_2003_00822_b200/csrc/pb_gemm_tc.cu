@@ -15,9 +15,14 @@
 // so every product is exactly 1.0 * (w_bit AND x_bit) and D[row][n] = C_in
 // exactly (f32 sums of ones, K < 2^24).  Sign handling, plane weights T_j and
 // layer weights S_i are applied in the exact int64 epilogue, as in the
-// POPC engine.  (A kind::i8 form with byte operands measured half the rate:
-// on sm_100a an M=128 MMA costs ~55 cycles for any N <= 64, so bits per MMA
-// decide throughput.)
+// POPC engine.
+//
+// Why this shape (measured on B200, scripts/tc_mb.cu): an M=128
+// tcgen05 MMA costs ~55 cycles for any N <= 64 (an M=256 CTA-pair MMA costs the
+// same on two SMs), so weight bits per MMA set the rate: kind::i8 with byte
+// operands carries 32 bits per row, kind::mxf4 nibbles carry 64.  The issuing
+// warp blocks on each MMA, so barrier round trips between MMAs are paid
+// serially; an A slot therefore holds 16 words (8 MMAs) per handshake.
 //
 // Work decomposition: stream-K over units (128-row tile, 32-word K-chunk);
 // each CTA (one per SM, persistent) walks a contiguous unit range.  For a row
@@ -30,15 +35,18 @@
 //
 // Warp roles (11 warps):
 //   warp 0      weight producer: TMA (cp.async.bulk.tensor.3d, 128B swizzle)
-//               of 128-row x 32-word bitlayer tiles into a 6-stage SMEM ring;
+//               of 128-row x 32-word bitlayer tiles into an 8-stage SMEM ring;
 //               starts before the activation kernel finishes (PDL);
-//   warp 1      TMEM allocator and single-thread MMA issuer;
+//   warp 1      TMEM allocator and MMA issuer (one elected lane);
 //   warp 2      B producer: 1-D bulk copies of the plane tiles (after PDL wait);
 //   warps 3..10 converters: thread = weight row; read the row's words from
-//               the swizzled SMEM tile, build A tiles, tcgen05.st them into an
-//               8-slot TMEM ring; warps 3..6 also run the epilogue.
+//               the swizzled SMEM tile, build A, tcgen05.st it into the TMEM A
+//               ring (software-pipelined: a slot is published while the next
+//               is built); warps 3..6 also run the epilogue.
 #include <cuda.h>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "pb_common.cuh"
@@ -50,17 +58,16 @@ namespace {
 constexpr int kConvWarps = 8;
 constexpr int kConv0 = 3;                     // first converter warp
 constexpr int kThreads = 32 * (kConv0 + kConvWarps);
-constexpr int kSlots = 7;                     // A ring: 7 slots x 32 TMEM columns (4 A tiles each)
-constexpr int kGroup = 8;                     // words per converter step (= 4 MMAs of K = 64)
-constexpr int kSfCol = 224;                   // block-scale factors (all 1.0): SFA 224.., SFB 232..
+constexpr int kMaxSlots = 8;                  // A ring: up to 8 slots x 64 TMEM columns (8 MMAs each)
+constexpr int kGroup = 16;                    // words per A slot
 constexpr int kChunkWords = 32;               // K-chunk = one 128-byte swizzle row
-constexpr int kWStages = 6;                   // weight tile ring
+constexpr int kWStages = 8;                   // weight tile ring
 constexpr uint32_t kWTileBytes = kTcRows * kChunkWords * 4;   // 16 KiB
-constexpr int kDCol = 256;                    // D accumulators start at TMEM column 256
-constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * (kChunkWords / 2) * 32 * 32;
+constexpr uint32_t kBStageMax = (kChunkWords / 2) * kTcMaxN * 32;   // 16 KiB
+constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * kBStageMax;
 
 struct Bars {
-    uint64_t a_full[kSlots], a_empty[kSlots];
+    uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
     uint64_t w_full[kWStages], w_empty[kWStages];
     uint64_t b_full[2], b_empty[2];
     uint64_t d_full, d_empty;
@@ -99,7 +106,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
         : "memory");
 }
-
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ void st_tmem_x32(uint32_t addr, const uint32_t (&v)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -126,14 +137,41 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Host-chosen decomposition.
+// 8 packed words -> 32 nibble registers (see the file header)
+__device__ __forceinline__ void build_a(const uint4 w0, const uint4 w1, uint32_t (&v)[32]) {
+    const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+    for (int uu = 0; uu < 8; ++uu) {
+        v[uu * 4 + 0] = ws[uu] & 0x11111111u;
+        v[uu * 4 + 1] = ws[uu] & 0x22222222u;
+        v[uu * 4 + 2] = ws[uu] & 0x44444444u;
+        v[uu * 4 + 3] = (ws[uu] >> 1) & 0x44444444u;
+    }
+}
+
+// Profiling (PB_TC_DEBUG=5): accumulate cycles spent in each wait site.
+#define TWAIT(bar, ph, slotid)                                   \
+    do {                                                         \
+        if (p.dbg == 5) {                                        \
+            const long long _t0 = clock64();                     \
+            mbar_wait(bar, ph);                                  \
+            prof[slotid] += clock64() - _t0;                     \
+        } else {                                                 \
+            mbar_wait(bar, ph);                                  \
+        }                                                        \
+    } while (0)
+
+// Host-chosen decomposition and TMEM map: [0, 64*slots) A ring, [sf_col, +16)
+// block-scale factors, [d_col, 512) one NPAD-column accumulator per layer.
 struct TcPlan {
     int tiles;        // ceil(R / 128)
     int chunks;       // 32-word K-chunks per tile
     long long units;  // tiles * chunks
+    int slots, sf_col, d_col;
+    int dbg;          // profiling knob (env PB_TC_DEBUG): 5 = print wait-cycle totals of CTA 0
 };
 
-// groups of 8 words in chunk kc (the last may hold only 4 real words; the TMA
+// groups of 16 words in chunk kc (the last may hold fewer real words; the TMA
 // zero-fills the rest, so its extra products are 0)
 __device__ __forceinline__ int chunk_groups(const GemmArgs& g, int kc) {
     int64_t n = g.kwords - (int64_t)kc * kChunkWords;
@@ -172,11 +210,15 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long G = gridDim.x;
+    long long prof[5] = {0, 0, 0, 0, 0};
+    const long long t_start = clock64();
+    long long g_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
     const long long u0 = p.units * blockIdx.x / G, u1 = p.units * (blockIdx.x + 1) / G;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kSlots; ++s) {
-            mbar_init(&bars.a_full[s], 4);
+        for (int s = 0; s < p.slots; ++s) {
+            mbar_init(&bars.a_full[s], 4);               // the 4 converter warps of one h-set
             mbar_init(&bars.a_empty[s], 1);
         }
         for (int s = 0; s < kWStages; ++s) {
@@ -206,7 +248,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const uint32_t s7 = 0x7F7F7F7Fu;
         asm volatile(
             "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
-                tmem + ((uint32_t)((warp & 3) * 32) << 16) + kSfCol),
+                tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)p.sf_col),
             "r"(s7)
             : "memory");
         tmem_st_wait();
@@ -218,15 +260,14 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
 
     if (warp == 0) {
         // ------------------------------------------------ weight tile producer (no PDL wait:
-        // the packed weights do not depend on the activation kernel).  Whole warp walks the
-        // schedule, one elected lane issues.
+        // the packed weights do not depend on the activation kernel)
         int tc = 0;
         for (long long u = u0; u < u1;) {
             const Seg sg = segment(p, u, u1);
             for (int kc = sg.kcA; kc < sg.kcB; ++kc)
                 for (int i = 0; i < g.k_used; ++i, ++tc) {
                     const int st = tc % kWStages;
-                    mbar_wait(&bars.w_empty[st], (uint32_t)(((tc / kWStages) & 1) ^ 1));
+                    TWAIT(&bars.w_empty[st], (uint32_t)(((tc / kWStages) & 1) ^ 1), 0);
                     if (elect_one()) {
                         mbar_arrive_expect_tx(&bars.w_full[st], kWTileBytes);
                         tma_load_3d(wtile0 + st * kWTileBytes, &wmap, kc * kChunkWords, sg.rt * kTcRows, i,
@@ -257,11 +298,11 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer: the whole warp walks the
         // schedule (warp-uniform values stay in uniform registers), one elected lane issues.
-        // kind::mxf4: A, B = E2M1 (1), scale format UE8M0 (bit 23), K = 64
+        // kind::mxf4: A, B = E2M1 (1), scale format UE8M0 (bit 23), K = 64, M = 128
         const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(NPAD >> 3) << 17) | (1u << 23) |
                                ((uint32_t)(kTcRows >> 4) << 24);
-        const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 8;
-        uint32_t gidx = 0;
+        const uint32_t sfa = tmem + p.sf_col, sfb = tmem + p.sf_col + 8;
+        uint32_t slot = 0, phase = 0;
         int cc = 0, seg = 0;
         for (long long u = u0; u < u1; ++seg) {
             const Seg sg = segment(p, u, u1);
@@ -269,28 +310,31 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             tc_fence_after();
             for (int kc = sg.kcA; kc < sg.kcB; ++kc, ++cc) {
                 const int st = cc & 1;
-                mbar_wait(&bars.b_full[st], (uint32_t)((cc >> 1) & 1));
+                TWAIT(&bars.b_full[st], (uint32_t)((cc >> 1) & 1), 1);
+                if (p.dbg == 6 && cc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof[0]));
                 tc_fence_after();
                 const uint64_t bdesc0 = b_desc(smem_u32(btile0 + st * kBStage));
                 const int ng = chunk_groups(g, kc);
                 for (int i = 0; i < g.k_used; ++i) {
-                    const uint32_t dcol = tmem + kDCol + (uint32_t)(i * NPAD);
-                    for (int grp = 0; grp < ng; ++grp, ++gidx) {
-                        const uint32_t slot = gidx % kSlots;
-                        mbar_wait(&bars.a_full[slot], (gidx / kSlots) & 1);
+                    const uint32_t dcol = tmem + (uint32_t)(p.d_col + i * NPAD);
+                    for (int grp = 0; grp < ng; ++grp) {
+                        TWAIT(&bars.a_full[slot], phase, 2);
                         tc_fence_after();
                         if (elect_one()) {
                             // descriptor start address advances in 16 B units: one B tile = NPAD*32 B
-                            const uint64_t bd = bdesc0 + (uint64_t)(grp * 4 * (kBTile / 16));
-                            const uint32_t a0 = tmem + slot * 32;
-                            const uint32_t acc0 = (kc == sg.kcA && grp == 0) ? 0u : 1u;
-                            tc_mma(dcol, a0, bd, idesc, acc0, sfa, sfb);
-                            tc_mma(dcol, a0 + 8, bd + (kBTile / 16), idesc, 1u, sfa, sfb);
-                            tc_mma(dcol, a0 + 16, bd + 2 * (kBTile / 16), idesc, 1u, sfa, sfb);
-                            tc_mma(dcol, a0 + 24, bd + 3 * (kBTile / 16), idesc, 1u, sfa, sfb);
+                            const uint64_t bd = bdesc0 + (uint64_t)(grp * 8 * (kBTile / 16));
+                            const uint32_t a0 = tmem + slot * 64;
+#pragma unroll
+                            for (int uu = 0; uu < 8; ++uu)
+                                tc_mma(dcol, a0 + 8 * uu, bd + uu * (kBTile / 16), idesc,
+                                       (uu == 0 && kc == sg.kcA && grp == 0) ? 0u : 1u, sfa, sfb);
                             tc_commit(&bars.a_empty[slot]);
                         }
                         __syncwarp();
+                        if (++slot == (uint32_t)p.slots) {
+                            slot = 0;
+                            phase ^= 1;
+                        }
                     }
                 }
                 if (elect_one()) tc_commit(&bars.b_empty[st]);
@@ -307,8 +351,23 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const int q = warp & 3;                // TMEM lane quarter this warp may access
         const int m = q * 32 + lane;           // row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const uint32_t wtile_s = smem_u32(wtile0) + (uint32_t)m * 128;
+        const uint32_t swz = (uint32_t)(m & 7);
         long long gidx = 0;
         int tc = 0, seg = 0;
+        // my groups are the global group indices g = h, h + 2, h + 4, ...
+        int slot = h, sphase = 0;
+        // software pipeline: the TMEM stores of one slot drain while the next is built
+        int pend_slot = -1;
+        auto publish = [&]() {
+            if (pend_slot >= 0) {
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars.a_full[pend_slot]);
+                pend_slot = -1;
+            }
+        };
         for (long long u = u0; u < u1; ++seg) {
             const Seg sg = segment(p, u, u1);
             const int64_t row = (int64_t)sg.rt * kTcRows + m;
@@ -317,36 +376,36 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 const int ng = chunk_groups(g, kc);
                 for (int i = 0; i < g.k_used; ++i, ++tc) {
                     const int st = tc % kWStages;
-                    mbar_wait(&bars.w_full[st], (uint32_t)((tc / kWStages) & 1));
-                    const uint8_t* trow = wtile0 + st * kWTileBytes + m * 128;
+                    TWAIT(&bars.w_full[st], (uint32_t)((tc / kWStages) & 1), 3);
+                    const uint32_t trow = wtile_s + (uint32_t)st * kWTileBytes;
                     for (int grp = (int)((h - (gidx & 1)) & 1); grp < ng; grp += 2) {
-                        const long long gi = gidx + grp;
                         // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
-                        const uint4 w0 = *reinterpret_cast<const uint4*>(trow + (((2 * grp) ^ (m & 7)) << 4));
-                        const uint4 w1 = *reinterpret_cast<const uint4*>(trow + (((2 * grp + 1) ^ (m & 7)) << 4));
-                        const int slot = (int)(gi % kSlots);
-                        mbar_wait(&bars.a_empty[slot], (uint32_t)(((gi / kSlots) & 1) ^ 1));
+                        const uint32_t c0 = 4u * (uint32_t)grp;
+                        const uint4 w0 = lds128(trow + (((c0 + 0) ^ swz) << 4));
+                        const uint4 w1 = lds128(trow + (((c0 + 1) ^ swz) << 4));
+                        const uint4 w2 = lds128(trow + (((c0 + 2) ^ swz) << 4));
+                        const uint4 w3 = lds128(trow + (((c0 + 3) ^ swz) << 4));
+                        uint32_t va[32], vb[32];
+                        build_a(w0, w1, va);
+                        build_a(w2, w3, vb);
+                        publish();                      // previous slot's A is in TMEM: tell the MMA
+                        TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
                         tc_fence_after();
-                        uint32_t v[32];
-                        const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-                        for (int uu = 0; uu < 8; ++uu) {
-                            v[uu * 4 + 0] = ws[uu] & 0x11111111u;
-                            v[uu * 4 + 1] = ws[uu] & 0x22222222u;
-                            v[uu * 4 + 2] = ws[uu] & 0x44444444u;
-                            v[uu * 4 + 3] = (ws[uu] >> 1) & 0x44444444u;
+                        st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 64), va);
+                        st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 64 + 32), vb);
+                        pend_slot = slot;
+                        slot += 2;
+                        if (slot >= p.slots) {
+                            slot -= p.slots;
+                            sphase ^= 1;
                         }
-                        st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 32), v);
-                        tmem_st_wait();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&bars.a_full[slot]);
                     }
-                    __syncwarp();
+                    __syncwarp();                       // this warp's words are in registers / TMEM
                     if (lane == 0) mbar_arrive(&bars.w_empty[st]);
                     gidx += ng;
                 }
             }
+            publish();
 
             if (h == 0) {
                 // ---------------- epilogue: fold D (k_used x NPAD) into exact int64
@@ -362,14 +421,15 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
 #pragma unroll
                     for (int c = 0; c < NPAD; c += 8) {
                         uint32_t t8[8];
-                        ld_tmem_x8(tmem + lane_off + kDCol + (uint32_t)(i * NPAD + c), t8);
+                        ld_tmem_x8(tmem + lane_off + (uint32_t)(p.d_col + i * NPAD + c), t8);
 #pragma unroll
                         for (int e = 0; e < 8; ++e) dv[c + e] = t8[e];
                     }
                     tmem_ld_wait();
                     const unsigned long long Si = layer_scale(g.L, g.offset, i);
 #pragma unroll
-                    for (int n = 0; n < NPAD; ++n) cs[n] += Si * (unsigned long long)__float2uint_rn(__uint_as_float(dv[n]));
+                    for (int n = 0; n < NPAD; ++n)
+                        cs[n] += Si * (unsigned long long)__float2uint_rn(__uint_as_float(dv[n]));
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -444,6 +504,17 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         }
     }
 
+    if (p.dbg == 5 && blockIdx.x == 0 && lane == 0)
+        printf("warp %d total %lld  w_empty %lld b_full %lld a_full %lld w_full %lld a_empty %lld\n", warp,
+               clock64() - t_start, prof[0], prof[1], prof[2], prof[3], prof[4]);
+    if (p.dbg == 6 && warp == 1 && lane == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        printf("cta %d sm %u units %lld cycles %lld end_ns %lld start_ns %lld firstb_ns %lld\n", blockIdx.x, smid,
+               u1 - u0, clock64() - t_start, gt, g_start, prof[0]);
+    }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -481,15 +552,20 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 {
     static int sms = 0;
     static bool attr = false;
+    static int dbg = -1;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const char* ev = getenv("PB_TC_DEBUG");
+        dbg = ev ? atoi(ev) : 0;
     }
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)kSmemBytes);
         if (e != cudaSuccess) return e;
+        cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
         attr = true;
     }
     CUtensorMap map;
@@ -499,6 +575,11 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
     p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
     p.units = (long long)p.tiles * p.chunks;
+    p.d_col = 512 - (g.k_used * NPAD + 31) / 32 * 32;
+    p.sf_col = p.d_col - 16;
+    p.slots = p.sf_col / 64;
+    if (p.slots > kMaxSlots) p.slots = kMaxSlots;
+    p.dbg = dbg;
     long long grid = p.units < sms ? p.units : sms;
     if (grid > kMaxCtas) grid = kMaxCtas;
 
@@ -519,6 +600,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 
 bool tc_supported(const GemmArgs& g)
 {
+    // k_used * N_pad <= 256 leaves room for >= 3 A slots beside the accumulators
     return g.npad > 0 && g.k_used * g.npad <= 256 && g.kwords > 0 && g.R > 0 && g.B > 0 &&
            (g.R + kTcRows - 1) / kTcRows <= kMaxTiles && g.L <= 16;
 }

@@ -229,6 +229,132 @@ __global__ void __launch_bounds__(160, 1) mma_vs_st(long long* out, int iters) {
     if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
 }
 
+// ping-pong between warp 1 (producer role) and warp 0 (MMA role) through two mbarriers;
+// KIND 0: plain arrive both ways; 1: return via tcgen05.commit (no MMA); 2: 4 MMAs + commit.
+template <int KIND>
+__global__ void __launch_bounds__(64, 1) pingpong(long long* out, int iters) {
+    __shared__ __align__(1024) uint8_t sB[16 * 32];
+    __shared__ __align__(8) uint64_t full, empty;
+    __shared__ uint32_t tb;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tb)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < 16 * 32; i += 64) sB[i] = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(&full, 1);
+        mbar_init(&empty, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t t = tb;
+    long long t0 = clock64();
+    if (w == 1) {
+        for (int i = 0; i < iters; ++i) {
+            if (i > 0) mbar_wait(&empty, (i - 1) & 1);
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full)) : "memory");
+        }
+        mbar_wait(&empty, (iters - 1) & 1);
+    } else {
+        const uint32_t idesc = (2u << 4) | ((uint32_t)(16 >> 3) << 17) | (8u << 24);
+        const uint64_t bd = desc(smem_u32(sB));
+        for (int i = 0; i < iters; ++i) {
+            mbar_wait(&full, i & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            if (lane == 0) {
+                if (KIND == 0) {
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty)) : "memory");
+                } else {
+                    if (KIND == 2)
+                        for (int q = 0; q < 4; ++q)
+                            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+                                             t + 256),
+                                         "r"(t + (uint32_t)(q * 8)), "l"(bd), "r"(idesc), "r"(1));
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                        smem_u32(&empty)));
+                }
+            }
+            __syncwarp();
+        }
+    }
+    long long t1 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 32) out[0] = t1 - t0;
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(t));
+}
+
+// cta_group::2 (M = 256 across a CTA pair) mxf4 TS rate, N = 16
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma2_rate(long long* out, int iters) {
+    __shared__ __align__(1024) uint8_t sB[256 * 32];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ uint32_t tb;
+    const int w = threadIdx.x >> 5;
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tb)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    for (int i = threadIdx.x; i < 256 * 32; i += 128) sB[i] = (uint8_t)0x22;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t t = tb;
+    const uint32_t s7 = 0x7F7F7F7Fu;
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                     t + ((uint32_t)(w * 32) << 16) + 480),
+                 "r"(s7));
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (rank == 0 && threadIdx.x == 0) {
+        const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) | (1u << 23) | (16u << 24);
+        const uint64_t bd = desc(smem_u32(sB));
+        long long t0 = clock64();
+        for (int i = 0; i < iters; ++i) {
+            const uint32_t acc = i > 0;
+            asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::mxf4.block_scale.scale_vec::2X [%0], [%1], %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+                             t + 256),
+                         "r"(t + (uint32_t)((i & 7) * 8)), "l"(bd), "r"(idesc), "r"(acc), "r"(t + 480), "r"(t + 488));
+        }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                         smem_u32(&bar)),
+                     "h"((uint16_t)3));
+        mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (blockIdx.x == 0) out[0] = t1 - t0;
+    }
+    if (rank == 1 && threadIdx.x == 0) mbar_wait(&bar, 0);
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(t));
+}
+
+template <class K>
+void run64(const char* name, K k, int iters) {
+    long long* d;
+    cudaMalloc(&d, 8);
+    k<<<148, 64>>>(d, iters);
+    k<<<148, 64>>>(d, iters);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h = 0;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    printf("%-36s %s cycles/roundtrip = %.1f\n", name, e == cudaSuccess ? "" : cudaGetErrorString(e), (double)h / iters);
+    cudaFree(d);
+}
+
 void run2(const char* name, void (*k)(long long*, int), int iters) {
     long long* d;
     cudaMalloc(&d, 16);
@@ -262,6 +388,20 @@ void run(const char* name, K k, int iters, double per) {
 
 int main() {
     const int it = 4096;
+    {
+        long long* d;
+        cudaMalloc(&d, 8);
+        mma2_rate<<<148, 128>>>(d, it);
+        mma2_rate<<<148, 128>>>(d, it);
+        cudaError_t e = cudaDeviceSynchronize();
+        long long h = 0;
+        cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+        printf("%-36s %s cycles/op = %.1f (M=256 over 2 SMs)\n", "mma mxf4 TS cta_group::2 N16",
+               e == cudaSuccess ? "" : cudaGetErrorString(e), (double)h / it);
+    }
+    run64("pingpong plain arrive", pingpong<0>, it);
+    run64("pingpong commit (no mma)", pingpong<1>, it);
+    run64("pingpong 4 mma + commit", pingpong<2>, it);
     run("mma mxf4 TS M128 N8", mma_rate_f4<8>, it, 1);
     run("mma mxf4 TS M128 N16", mma_rate_f4<16>, it, 1);
     run("mma mxf4 TS M128 N32", mma_rate_f4<32>, it, 1);
