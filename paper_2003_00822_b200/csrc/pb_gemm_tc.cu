@@ -12,22 +12,25 @@
 //     ALU ops per 32 columns; stored with tcgen05.st.32x32b (lane = row);
 //   B (SMEM, N_pad plane rows x 32 bytes per 64 columns): the same nibble
 //     positions hold plane bits times {2, 1, 0.5, 0.5}[r] (pb_act.cu);
-// so every product is exactly 1.0 * (w_bit AND x_bit) and D[row][n] = C_in
-// exactly (f32 sums of ones, K < 2^24).  Sign handling, plane weights T_j and
-// layer weights S_i are applied in the exact int64 epilogue, as in the
-// POPC engine.
+// so every product is exactly 1.0 * (w_bit AND x_bit).  The layer weights
+// S_i = 2^(L-1-i) of the magnitude bitlayers ride on the E8M0 block
+// scale of B (2^s, exact), so all magnitude layers of a group accumulate into
+// one TMEM accumulator D_g = sum_i 2^(s_i) C_i, exact in f32 while
+// K * 2^G < 2^24 (G = layers per group); the sign layer (negative S_0) has its
+// own accumulator.  Plane weights T_j, the group weights and S_0 are applied in
+// the exact int64 epilogue, as in the POPC engine.
 //
 // Why this shape (measured on B200, scripts/tc_mb.cu): an M=128
 // tcgen05 MMA costs ~55 cycles for any N <= 64 (an M=256 CTA-pair MMA costs the
 // same on two SMs), so weight bits per MMA set the rate: kind::i8 with byte
 // operands carries 32 bits per row, kind::mxf4 nibbles carry 64.  The issuing
 // warp blocks on each MMA, so barrier round trips between MMAs are paid
-// serially; an A slot therefore holds 16 words (8 MMAs) per handshake.
+// serially; an A slot therefore holds a whole 32-word tile row (16 MMAs) per
+// handshake, and the two converter h-sets take alternate tiles.
 //
 // Work decomposition: stream-K over units (128-row tile, 32-word K-chunk);
-// each CTA (one per SM, persistent) walks a contiguous unit range.  For a row
-// tile every layer i < k_used has its own TMEM accumulator (k_used * N_pad
-// columns), so each B chunk staged in SMEM serves all layers.  A CTA that
+// each CTA (one per SM, persistent) walks a contiguous unit range; each B chunk
+// staged in SMEM serves all k_used layers of the chunk.  A CTA that
 // covers a whole tile writes y directly; a CTA holding part of a tile parks
 // its int64 sums in its own slot and bumps the tile's arrival counter; the
 // last arriving CTA sums the slots of all contributors (fixed order, exact)
@@ -55,19 +58,21 @@
 namespace pb {
 namespace {
 
-constexpr int kConvWarps = 8;
+constexpr int kConvWarps = 8;                 // 2 h-sets of 4 warps (one per TMEM lane quarter)
+constexpr int kHSets = kConvWarps / 4;
 constexpr int kConv0 = 3;                     // first converter warp
 constexpr int kThreads = 32 * (kConv0 + kConvWarps);
-constexpr int kMaxSlots = 8;                  // A ring: up to 8 slots x 64 TMEM columns (8 MMAs each)
-constexpr int kGroup = 16;                    // words per A slot
+constexpr int kMaxSlots = 4;                  // A ring: up to 4 slots x 128 TMEM columns (16 MMAs each)
+constexpr int kMaxRegions = 4;                // TMEM accumulators: sign layer + magnitude groups
 constexpr int kChunkWords = 32;               // K-chunk = one 128-byte swizzle row
 constexpr int kWStages = 8;                   // weight tile ring
 constexpr uint32_t kWTileBytes = kTcRows * kChunkWords * 4;   // 16 KiB
 constexpr uint32_t kBStageMax = (kChunkWords / 2) * kTcMaxN * 32;   // 16 KiB
-constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * kBStageMax;
+constexpr uint32_t kTotBytes = kTcMaxN * kTcRows * 8;          // epilogue per-row, per-batch int64 sums
+constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * kBStageMax + kTotBytes;
 
 struct Bars {
-    uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
+    uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];   // a_full: the 4 warps of one h-set
     uint64_t w_full[kWStages], w_empty[kWStages];
     uint64_t b_full[2], b_empty[2];
     uint64_t d_full, d_empty;
@@ -152,7 +157,7 @@ __device__ __forceinline__ void build_a(const uint4 w0, const uint4 w1, uint32_t
 // Profiling (PB_TC_DEBUG=5): accumulate cycles spent in each wait site.
 #define TWAIT(bar, ph, slotid)                                   \
     do {                                                         \
-        if (p.dbg == 5) {                                        \
+        if (p.prof) {                                            \
             const long long _t0 = clock64();                     \
             mbar_wait(bar, ph);                                  \
             prof[slotid] += clock64() - _t0;                     \
@@ -161,22 +166,38 @@ __device__ __forceinline__ void build_a(const uint4 w0, const uint4 w1, uint32_t
         }                                                        \
     } while (0)
 
-// Host-chosen decomposition and TMEM map: [0, 64*slots) A ring, [sf_col, +16)
-// block-scale factors, [d_col, 512) one NPAD-column accumulator per layer.
+// Host-chosen decomposition and TMEM map: [0, 128*slots) A ring,
+// [sf_col, sf_col + 64): columns 0..3 = SFA (1.0), columns 4(1+s).. = SFB 2^s
+// (scale-factor operands are addressed at 4-column granularity);
+// [d_col, d_col + regions*NPAD): accumulators (region 0 = sign layer).
 struct TcPlan {
     int tiles;        // ceil(R / 128)
     int chunks;       // 32-word K-chunks per tile
     long long units;  // tiles * chunks
     int slots, sf_col, d_col;
-    int dbg;          // profiling knob (env PB_TC_DEBUG): 5 = print wait-cycle totals of CTA 0
+    int G;            // magnitude layers per accumulator group (K * 2^G < 2^24)
+    int regions;      // 1 + ceil((k_used - 1) / G)
+    int dbg;          // profiling knob (env PB_TC_DEBUG): 1 = no A store, 2 = no MMA, 3 = neither,
+                      // 6 = per-CTA timeline
+    int prof;         // env PB_TC_PROF: print wait-cycle totals of CTA 0
 };
 
-// groups of 16 words in chunk kc (the last may hold fewer real words; the TMA
-// zero-fills the rest, so its extra products are 0)
-__device__ __forceinline__ int chunk_groups(const GemmArgs& g, int kc) {
-    int64_t n = g.kwords - (int64_t)kc * kChunkWords;
-    if (n > kChunkWords) n = kChunkWords;
-    return (int)((n + kGroup - 1) / kGroup);
+// Accumulator region of layer i, its block-scale exponent s (weight 2^s inside
+// the region) and whether i opens its region (first MMA overwrites).
+__device__ __forceinline__ void layer_region(const TcPlan& p, int k_used, int i, int& region, int& s, bool& first) {
+    if (i == 0) {
+        region = 0;
+        s = 0;
+        first = true;
+        return;
+    }
+    const int gi = (i - 1) / p.G;
+    const int lo = 1 + gi * p.G;                  // first (most significant) layer of the group
+    int hi = lo + p.G - 1;                        // last layer of the group
+    if (hi > k_used - 1) hi = k_used - 1;
+    region = 1 + gi;
+    s = hi - i;
+    first = (i == lo);
 }
 
 // A CTA's units [u0, u1) split into segments of one row tile: [kcA, kcB) of tile rt.
@@ -205,8 +226,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     Bars& bars = *reinterpret_cast<Bars*>(smem);
     uint8_t* wtile0 = smem + 1024;
     uint8_t* btile0 = wtile0 + kWStages * kWTileBytes;
+    unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(btile0 + 2 * kBStageMax);  // [b][128]
     constexpr uint32_t kBTile = NPAD * 32;                    // one MMA's B (64 columns)
-    constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;  // one K-chunk
+    constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;  // one K-chunk (16 MMAs)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long G = gridDim.x;
@@ -223,7 +245,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         }
         for (int s = 0; s < kWStages; ++s) {
             mbar_init(&bars.w_full[s], 1);
-            mbar_init(&bars.w_empty[s], kConvWarps);
+            mbar_init(&bars.w_empty[s], 4);              // the h-set that converts the tile
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars.b_full[s], 1);
@@ -244,13 +266,23 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     tc_fence_after();
     const uint32_t tmem = bars.tmem_base;
     if (warp >= kConv0 && warp < kConv0 + 4) {
-        // E8M0 block scale factors = 1.0 (0x7F) for SFA and SFB, all 128 lanes
-        const uint32_t s7 = 0x7F7F7F7Fu;
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
-                tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)p.sf_col),
-            "r"(s7)
-            : "memory");
+        // E8M0 block scale factors: columns 0..3 = 1.0 (SFA), columns 4(1+s)..4(1+s)+3 = 2^s
+        // (SFB of layers with in-group weight 2^s); every byte of a column holds the same value
+#pragma unroll
+        for (int blk = 0; blk < 4; ++blk) {
+            uint32_t v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const int col = blk * 16 + c, sidx = col / 4;   // sidx 0 = SFA, 1 + s = 2^s
+                v[c] = 0x01010101u * (uint32_t)(127 + (sidx == 0 ? 0 : sidx - 1));
+            }
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                    tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(p.sf_col + blk * 16)),
+                "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+                "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+                : "memory");
+        }
         tmem_st_wait();
     }
     tc_fence_before();
@@ -287,9 +319,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 const int st = cc & 1;
                 mbar_wait(&bars.b_empty[st], (uint32_t)(((cc >> 1) & 1) ^ 1));
                 if (elect_one()) {
-                    const uint32_t bytes = (uint32_t)chunk_groups(g, kc) * (kGroup / 2) * kBTile;
-                    mbar_arrive_expect_tx(&bars.b_full[st], bytes);
-                    bulk_g2s(btile0 + st * kBStage, g.bexp + (int64_t)kc * kBStage, bytes, &bars.b_full[st]);
+                    mbar_arrive_expect_tx(&bars.b_full[st], kBStage);
+                    bulk_g2s(btile0 + st * kBStage, g.bexp + (int64_t)kc * kBStage, kBStage, &bars.b_full[st]);
                 }
                 __syncwarp();
             }
@@ -301,7 +332,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // kind::mxf4: A, B = E2M1 (1), scale format UE8M0 (bit 23), K = 64, M = 128
         const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(NPAD >> 3) << 17) | (1u << 23) |
                                ((uint32_t)(kTcRows >> 4) << 24);
-        const uint32_t sfa = tmem + p.sf_col, sfb = tmem + p.sf_col + 8;
+        const uint32_t sfa = tmem + p.sf_col;
         uint32_t slot = 0, phase = 0;
         int cc = 0, seg = 0;
         for (long long u = u0; u < u1; ++seg) {
@@ -311,30 +342,32 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             for (int kc = sg.kcA; kc < sg.kcB; ++kc, ++cc) {
                 const int st = cc & 1;
                 TWAIT(&bars.b_full[st], (uint32_t)((cc >> 1) & 1), 1);
-                if (p.dbg == 6 && cc == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof[0]));
                 tc_fence_after();
                 const uint64_t bdesc0 = b_desc(smem_u32(btile0 + st * kBStage));
-                const int ng = chunk_groups(g, kc);
                 for (int i = 0; i < g.k_used; ++i) {
-                    const uint32_t dcol = tmem + (uint32_t)(p.d_col + i * NPAD);
-                    for (int grp = 0; grp < ng; ++grp) {
-                        TWAIT(&bars.a_full[slot], phase, 2);
-                        tc_fence_after();
-                        if (elect_one()) {
-                            // descriptor start address advances in 16 B units: one B tile = NPAD*32 B
-                            const uint64_t bd = bdesc0 + (uint64_t)(grp * 8 * (kBTile / 16));
-                            const uint32_t a0 = tmem + slot * 64;
+                    int region, sexp;
+                    bool first;
+                    layer_region(p, g.k_used, i, region, sexp, first);
+                    const uint32_t dcol = tmem + (uint32_t)(p.d_col + region * NPAD);
+                    const uint32_t sfb = tmem + (uint32_t)(p.sf_col + 4 * (1 + sexp));
+                    const bool open = first && kc == sg.kcA;
+                    TWAIT(&bars.a_full[slot], phase, 2);
+                    tc_fence_after();
+                    if (p.dbg == 2 || p.dbg == 3) {
+                        if (elect_one()) tc_commit(&bars.a_empty[slot]);
+                    } else if (elect_one()) {
+                        // descriptor start address advances in 16 B units: one B tile = NPAD*32 B
+                        const uint32_t a0 = tmem + slot * 128;
 #pragma unroll
-                            for (int uu = 0; uu < 8; ++uu)
-                                tc_mma(dcol, a0 + 8 * uu, bd + uu * (kBTile / 16), idesc,
-                                       (uu == 0 && kc == sg.kcA && grp == 0) ? 0u : 1u, sfa, sfb);
-                            tc_commit(&bars.a_empty[slot]);
-                        }
-                        __syncwarp();
-                        if (++slot == (uint32_t)p.slots) {
-                            slot = 0;
-                            phase ^= 1;
-                        }
+                        for (int uu = 0; uu < 16; ++uu)
+                            tc_mma(dcol, a0 + 8 * uu, bdesc0 + uu * (kBTile / 16), idesc,
+                                   (uu == 0 && open) ? 0u : 1u, sfa, sfb);
+                        tc_commit(&bars.a_empty[slot]);
+                    }
+                    __syncwarp();
+                    if (++slot == (uint32_t)p.slots) {
+                        slot = 0;
+                        phase ^= 1;
                     }
                 }
                 if (elect_one()) tc_commit(&bars.b_empty[st]);
@@ -347,17 +380,17 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     } else {
         // ------------------------------------------------ converters (+ epilogue)
         const int cw = warp - kConv0;
-        const int h = cw >> 2;                 // 0: warps 3..6, 1: warps 7..10
+        const int h = cw >> 2;                 // h-set: 0 = warps 3..6 (also the epilogue), 1 = warps 7..10
         const int q = warp & 3;                // TMEM lane quarter this warp may access
         const int m = q * 32 + lane;           // row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const uint32_t wtile_s = smem_u32(wtile0) + (uint32_t)m * 128;
         const uint32_t swz = (uint32_t)(m & 7);
-        long long gidx = 0;
         int tc = 0, seg = 0;
-        // my groups are the global group indices g = h, h + 2, h + 4, ...
-        int slot = h, sphase = 0;
-        // software pipeline: the TMEM stores of one slot drain while the next is built
+        // tiles (kc, i) in issue order; h-set h converts tiles t = h, h + 2, ...; tile t uses
+        // A slot t % slots
+        int slot = h % p.slots, sphase = (h / p.slots) & 1;
+        // software pipeline: the TMEM stores of one tile drain while the next is awaited
         int pend_slot = -1;
         auto publish = [&]() {
             if (pend_slot >= 0) {
@@ -373,77 +406,74 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             const int64_t row = (int64_t)sg.rt * kTcRows + m;
             const bool row_ok = row < g.R;
             for (int kc = sg.kcA; kc < sg.kcB; ++kc) {
-                const int ng = chunk_groups(g, kc);
                 for (int i = 0; i < g.k_used; ++i, ++tc) {
+                    if ((tc & 1) != h) continue;
                     const int st = tc % kWStages;
                     TWAIT(&bars.w_full[st], (uint32_t)((tc / kWStages) & 1), 3);
                     const uint32_t trow = wtile_s + (uint32_t)st * kWTileBytes;
-                    for (int grp = (int)((h - (gidx & 1)) & 1); grp < ng; grp += 2) {
-                        // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
-                        const uint32_t c0 = 4u * (uint32_t)grp;
-                        const uint4 w0 = lds128(trow + (((c0 + 0) ^ swz) << 4));
-                        const uint4 w1 = lds128(trow + (((c0 + 1) ^ swz) << 4));
-                        const uint4 w2 = lds128(trow + (((c0 + 2) ^ swz) << 4));
-                        const uint4 w3 = lds128(trow + (((c0 + 3) ^ swz) << 4));
-                        uint32_t va[32], vb[32];
-                        build_a(w0, w1, va);
-                        build_a(w2, w3, vb);
-                        publish();                      // previous slot's A is in TMEM: tell the MMA
-                        TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
-                        tc_fence_after();
-                        st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 64), va);
-                        st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 64 + 32), vb);
-                        pend_slot = slot;
-                        slot += 2;
-                        if (slot >= p.slots) {
-                            slot -= p.slots;
-                            sphase ^= 1;
+                    publish();                          // previous tile's A is in TMEM: tell the MMA
+                    TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
+                    tc_fence_after();
+                    if (p.dbg != 7) {
+#pragma unroll 1
+                        for (int b4 = 0; b4 < 4; ++b4) {
+                            // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
+                            const uint4 w0 = lds128(trow + ((((uint32_t)(2 * b4)) ^ swz) << 4));
+                            const uint4 w1 = lds128(trow + ((((uint32_t)(2 * b4 + 1)) ^ swz) << 4));
+                            uint32_t v[32];
+                            build_a(w0, w1, v);
+                            if (p.dbg != 1 && p.dbg != 3)
+                                st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 128 + 32 * b4), v);
+                            else if (v[0] == 0x12345 && v[3] == 0x777)
+                                asm volatile("trap;");   // keep the ALU work alive
                         }
                     }
-                    __syncwarp();                       // this warp's words are in registers / TMEM
+                    __syncwarp();                       // this warp's words are in TMEM-bound registers
                     if (lane == 0) mbar_arrive(&bars.w_empty[st]);
-                    gidx += ng;
+                    pend_slot = slot;
+                    slot += 2;
+                    while (slot >= p.slots) {
+                        slot -= p.slots;
+                        sphase ^= 1;
+                    }
                 }
             }
             publish();
 
             if (h == 0) {
-                // ---------------- epilogue: fold D (k_used x NPAD) into exact int64
+                // ---------------- epilogue: fold the accumulators into exact int64
                 mbar_wait(&bars.d_full, (uint32_t)(seg & 1));
                 tc_fence_after();
                 pdl_wait();
-                // cs[n] = sum_i S_i * C_in  (D holds C_in as an exact f32)
-                unsigned long long cs[NPAD];
-#pragma unroll
-                for (int n = 0; n < NPAD; ++n) cs[n] = 0;
-                for (int i = 0; i < g.k_used; ++i) {
-                    uint32_t dv[NPAD];
-#pragma unroll
+                // tot_b = sum_j T_j sum_r w_r D_r[b*a + j]; region weights: S_0 for the sign
+                // layer, S_hi (its least significant layer) for a magnitude group
+                for (int b = 0; b < g.B; ++b) s_tot[b * kTcRows + m] = 0;
+                for (int r = 0; r < p.regions; ++r) {
+                    int hi = 0;
+                    if (r > 0) {
+                        hi = r * p.G;
+                        if (hi > g.k_used - 1) hi = g.k_used - 1;
+                    }
+                    const unsigned long long wr = layer_scale(g.L, g.offset, hi);
+#pragma unroll 1
                     for (int c = 0; c < NPAD; c += 8) {
                         uint32_t t8[8];
-                        ld_tmem_x8(tmem + lane_off + (uint32_t)(p.d_col + i * NPAD + c), t8);
+                        ld_tmem_x8(tmem + lane_off + (uint32_t)(p.d_col + r * NPAD + c), t8);
+                        tmem_ld_wait();
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) dv[c + e] = t8[e];
+                        for (int e = 0; e < 8; ++e) {
+                            const int n = c + e, b = n / g.a, j = n - b * g.a;
+                            if (b < g.B)
+                                s_tot[b * kTcRows + m] +=
+                                    plane_scale(g.a, j) *
+                                    (wr * (unsigned long long)__float2uint_rn(__uint_as_float(t8[e])));
+                        }
                     }
-                    tmem_ld_wait();
-                    const unsigned long long Si = layer_scale(g.L, g.offset, i);
-#pragma unroll
-                    for (int n = 0; n < NPAD; ++n)
-                        cs[n] += Si * (unsigned long long)__float2uint_rn(__uint_as_float(dv[n]));
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.d_empty);
-                // tot_b = sum_j T_j cs[b*a + j]
-                auto tot_of = [&](int b) -> unsigned long long {
-                    unsigned long long t = 0;
-#pragma unroll
-                    for (int n = 0; n < NPAD; ++n) {
-                        const int j = n - b * g.a;
-                        if (j >= 0 && j < g.a) t += plane_scale(g.a, j) * cs[n];
-                    }
-                    return t;
-                };
+                auto tot_of = [&](int b) -> unsigned long long { return s_tot[b * kTcRows + m]; };
                 const bool whole = (sg.kcA == 0 && sg.kcB == p.chunks);
                 bool finalize = whole;
                 if (!whole) {
@@ -504,7 +534,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         }
     }
 
-    if (p.dbg == 5 && blockIdx.x == 0 && lane == 0)
+    if (p.prof && blockIdx.x == 0 && lane == 0)
         printf("warp %d total %lld  w_empty %lld b_full %lld a_full %lld w_full %lld a_empty %lld\n", warp,
                clock64() - t_start, prof[0], prof[1], prof[2], prof[3], prof[4]);
     if (p.dbg == 6 && warp == 1 && lane == 0) {
@@ -512,8 +542,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         long long gt;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        printf("cta %d sm %u units %lld cycles %lld end_ns %lld start_ns %lld firstb_ns %lld\n", blockIdx.x, smid,
-               u1 - u0, clock64() - t_start, gt, g_start, prof[0]);
+        printf("cta %d sm %u units %lld cycles %lld end_ns %lld start_ns %lld\n", blockIdx.x, smid, u1 - u0,
+               clock64() - t_start, gt, g_start);
     }
     tc_fence_before();
     __syncthreads();
@@ -547,18 +577,48 @@ cudaError_t make_weight_map(const GemmArgs& g, CUtensorMap* map)
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+int ceil_log2_i(int64_t v) {
+    int k = 0;
+    while (((int64_t)1 << k) < v) ++k;
+    return k;
+}
+
+// The plan for a shape, or false when the tensor engine does not cover it.
+bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
+{
+    if (npad <= 0 || g.kwords <= 0 || g.R <= 0 || g.B <= 0 || g.L > 16) return false;
+    p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
+    if (p.tiles > kMaxTiles) return false;
+    p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
+    p.units = (long long)p.tiles * p.chunks;
+    // exact f32 accumulation: a group sum is < K * 2^G <= 2^24
+    p.G = 24 - ceil_log2_i(g.kwords * 32);
+    if (p.G > 15) p.G = 15;                       // 15 SFB scale values fit the 64-column SF area
+    if (p.G < 1) return false;
+    p.regions = 1 + (g.k_used - 1 + p.G - 1) / p.G;
+    if (p.regions > kMaxRegions) return false;
+    p.d_col = 512 - (p.regions * npad + 31) / 32 * 32;
+    p.sf_col = p.d_col - 64;
+    p.slots = p.sf_col / 128;
+    if (p.slots > kMaxSlots) p.slots = kMaxSlots;
+    if (p.slots < 2) return false;
+    return true;
+}
+
 template <int NPAD>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 {
     static int sms = 0;
     static bool attr = false;
-    static int dbg = -1;
+    static int dbg = -1, prof = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const char* ev = getenv("PB_TC_DEBUG");
         dbg = ev ? atoi(ev) : 0;
+        ev = getenv("PB_TC_PROF");
+        prof = ev ? atoi(ev) : 0;
     }
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -568,18 +628,13 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
                              (int)cudaSharedmemCarveoutMaxShared);
         attr = true;
     }
+    TcPlan p;
+    if (!make_plan(g, NPAD, p)) return cudaErrorNotSupported;
     CUtensorMap map;
     cudaError_t e = make_weight_map(g, &map);
     if (e != cudaSuccess) return e;
-    TcPlan p;
-    p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
-    p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
-    p.units = (long long)p.tiles * p.chunks;
-    p.d_col = 512 - (g.k_used * NPAD + 31) / 32 * 32;
-    p.sf_col = p.d_col - 16;
-    p.slots = p.sf_col / 64;
-    if (p.slots > kMaxSlots) p.slots = kMaxSlots;
     p.dbg = dbg;
+    p.prof = prof;
     long long grid = p.units < sms ? p.units : sms;
     if (grid > kMaxCtas) grid = kMaxCtas;
 
@@ -600,9 +655,8 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 
 bool tc_supported(const GemmArgs& g)
 {
-    // k_used * N_pad <= 256 leaves room for >= 3 A slots beside the accumulators
-    return g.npad > 0 && g.k_used * g.npad <= 256 && g.kwords > 0 && g.R > 0 && g.B > 0 &&
-           (g.R + kTcRows - 1) / kTcRows <= kMaxTiles && g.L <= 16;
+    TcPlan p;
+    return make_plan(g, g.npad, p);
 }
 
 cudaError_t launch_gemm_tc(const GemmArgs& g, cudaStream_t s)

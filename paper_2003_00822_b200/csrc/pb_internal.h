@@ -29,7 +29,7 @@ inline int tc_npad(int64_t batch, int32_t a) {
 //   [partial slots int64 x kMaxCtas x 2 x B x 128]   tensor engine only
 //   [f_b int32 x B][Σx_q partials int64 x B x 64][bit planes [B][a][kwords]]
 //   [tensor-engine B operand tiles: one N_pad x 32-byte e2m1 tile per 2 words
-//    (64 columns), kwords rounded up to 8 words]
+//    (64 columns), kwords rounded up to 32 words]
 // Every region except the counters is fully rewritten by each call, so one
 // zero-filled workspace can serve calls of any shape (not concurrently).
 constexpr int kMaxTiles = 8192;      // tensor engine: rows <= 8192 * 128
@@ -48,7 +48,7 @@ inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     l.off_xsum = align_up(l.off_f + sizeof(int32_t) * (size_t)batch);
     l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kMaxSplit);
     l.off_bexp = align_up(l.off_planes + sizeof(uint32_t) * (size_t)batch * act_bits * kwords);
-    l.total = align_up(l.off_bexp + (size_t)((kwords + 7) / 8 * 8) * 16 * (size_t)l.npad);
+    l.total = align_up(l.off_bexp + (size_t)((kwords + 31) / 32 * 32) * 16 * (size_t)l.npad);
     return l;
 }
 
