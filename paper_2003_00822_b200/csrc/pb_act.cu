@@ -9,9 +9,11 @@
 // B operand (tcgen05 kind::mxf4, packed e2m1, K-major no-swizzle canonical
 // layout): per 2 words (64 columns) one N_pad x 32-byte tile.  The 16 bytes
 // of word w in plane row n are 4 uint32 (r = 0..3) whose nibble e holds
-// X_n bit (4e + r) times the e2m1 code {2.0, 1.0, 0.5, 0.5}[r]; against the
-// weight nibbles {0.5, 1.0, 2.0, 2.0}[r] * w_bit (pb_gemm_tc.cu) every 0/1
-// product is exactly 1.0.
+// X_n bit (4e + r) as the e2m1 code 2.0 (0b0100); against a weight nibble
+// 1.0 * hi_bit + 0.5 * lo_bit (pb_gemm_tc.cu) the product is exactly
+// (2 hi + lo) * x_bit.  Words in [kwords, roundup(kwords, 32)) -- the K tail
+// of the last 32-word chunk -- get zero B so that the chunk tail contributes
+// nothing whatever the weight operand holds there.
 //
 // Grid: (nsplit, B) CTAs of 512 threads.  Every CTA recomputes max|x[b,:]|
 // (an L2-resident re-read of K floats) so no second launch or grid sync is
@@ -91,6 +93,7 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
     const int64_t w0 = (int64_t)blockIdx.x * words_per_cta;
     int64_t w1 = w0 + words_per_cta;
     if (w1 > kwords) w1 = kwords;
+    if (npad && blockIdx.x == gridDim.x - 1) w1 = (kwords + 31) / 32 * 32;   // zero B for the chunk tail
     uint32_t* pb = planes + (int64_t)b * a * kwords;
     long long xs = 0;
     for (int64_t w = w0 + warp; w < w1; w += kWarps) {
@@ -105,7 +108,7 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
             const uint32_t word = __ballot_sync(0xffffffffu, (unsigned)((q >> (a - 1 - j)) & 1));
             if (lane == j) mine = word;
         }
-        if (lane < a) pb[(int64_t)lane * kwords + w] = mine;
+        if (lane < a && w < kwords) pb[(int64_t)lane * kwords + w] = mine;
         if (npad) {
             // tile (w / 2), k-half (w % 2); lane j < a writes plane row n = b*a + j
             uint8_t* tile = bexp + (int64_t)(w >> 1) * npad * 32 + (w & 1) * 128;
@@ -114,8 +117,8 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
                 *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + (n & 7) * 16) = v;
             };
             if (lane < a)
-                put(b * a + lane, make_uint4(((p >> 0) & 0x11111111u) * 4u, ((p >> 1) & 0x11111111u) * 2u,
-                                             (p >> 2) & 0x11111111u, (p >> 3) & 0x11111111u));
+                put(b * a + lane, make_uint4(((p >> 0) & 0x11111111u) << 2, ((p >> 1) & 0x11111111u) << 2,
+                                             ((p >> 2) & 0x11111111u) << 2, ((p >> 3) & 0x11111111u) << 2));
             if (b == (int)gridDim.y - 1) {   // zero padding rows n in [a*B, npad)
                 const int n = (int)gridDim.y * a + lane;
                 if (n < npad) put(n, make_uint4(0u, 0u, 0u, 0u));

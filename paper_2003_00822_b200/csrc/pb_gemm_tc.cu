@@ -2,31 +2,35 @@
 //
 // The 0/1 products of P:205-206 (W_i[r,c] AND X_j[b,c], summed over c) are
 // computed by tcgen05.mma.kind::mxf4.block_scale (packed e2m1 x e2m1 -> f32,
-// SASS UTCOMMA, all E8M0 block scales = 1.0) with both operands holding
-// single bits:
-//   A (TMEM, M = 128 rows x K = 64 e2m1 = 32 bytes): one packed weight word
-//     w (32 columns of one bitlayer row) becomes 4 registers of 8 nibbles,
-//       w & 0x11111111 (0.5), w & 0x22222222 (1.0), w & 0x44444444 (2.0),
-//       (w >> 1) & 0x44444444 (2.0),
-//     so nibble e of register r is bit(4e + r) times {0.5, 1, 2, 2}[r] -- five
-//     ALU ops per 32 columns; stored with tcgen05.st.32x32b (lane = row);
-//   B (SMEM, N_pad plane rows x 32 bytes per 64 columns): the same nibble
-//     positions hold plane bits times {2, 1, 0.5, 0.5}[r] (pb_act.cu);
-// so every product is exactly 1.0 * (w_bit AND x_bit).  The layer weights
-// S_i = 2^(L-1-i) of the magnitude bitlayers ride on the E8M0 block
-// scale of B (2^s, exact), so all magnitude layers of a group accumulate into
-// one TMEM accumulator D_g = sum_i 2^(s_i) C_i, exact in f32 while
-// K * 2^G < 2^24 (G = layers per group); the sign layer (negative S_0) has its
-// own accumulator.  Plane weights T_j, the group weights and S_0 are applied in
+// SASS UTCOMMA) with TWO adjacent bitlayers stacked in every A nibble -- the
+// "multiple bitlayers may be stacked together" option of P:206:
+//   * e2m1 nibbles 0b00hl are exactly 1.0*h + 0.5*l, so the nibble of column
+//     c holds the bits of layers (i, i+1) of column c; B holds each plane bit
+//     as 2.0 (pb_act.cu), so every product is (2 W_i + W_{i+1}) * x_bit --
+//     the two layers' relative weight S_i / S_{i+1} = 2;
+//   * the sign layer (S_0 < 0) is carried as its complement with weight
+//     |S_0| plus the exact correction -|S_0| * sum_c x_q (since
+//     -|S_0| s = |S_0| (1 - s) - |S_0|), so every layer weight is a positive
+//     power of two and the layers pair up as (0,1), (2,3), ...;
+//   * the passes of a group ride on the E8M0 block scale of B (2^s, exact),
+//     so a whole group accumulates into one TMEM accumulator
+//     D_g = sum_pass 2^s (2 C_hi + C_lo), exact in f32 while K * 2^G <= 2^24
+//     (G = layers per group).
+// Plane weights T_j, the group weights and the sign correction are applied in
 // the exact int64 epilogue, as in the POPC engine.
+//
+// Building A (per pair of words hi, lo and register r = 0..3, nibble e =
+// column 4e + r):  ((hi >> (r-1)) & 0x22222222) | ((lo >> r) & 0x11111111),
+// stored with tcgen05.st.32x32b (lane = row).
 //
 // Why this shape (measured on B200, scripts/tc_mb.cu): an M=128
 // tcgen05 MMA costs ~55 cycles for any N <= 64 (an M=256 CTA-pair MMA costs the
 // same on two SMs), so weight bits per MMA set the rate: kind::i8 with byte
-// operands carries 32 bits per row, kind::mxf4 nibbles carry 64.  The issuing
-// warp blocks on each MMA, so barrier round trips between MMAs are paid
-// serially; an A slot therefore holds a whole 32-word tile row (16 MMAs) per
-// handshake, and the two converter h-sets take alternate tiles.
+// operands carries 32 bits per row, kind::mxf4 nibbles with one layer carry
+// 64, two stacked layers 128.  The issuing warp blocks on each MMA, so
+// barrier round trips between MMAs are paid serially; an A slot therefore
+// holds a whole 32-word pass (16 MMAs) per handshake, and the two converter
+// h-sets take alternate passes.
 //
 // Work decomposition: stream-K over units (128-row tile, 32-word K-chunk);
 // each CTA (one per SM, persistent) walks a contiguous unit range; each B chunk
@@ -42,10 +46,11 @@
 //               starts before the activation kernel finishes (PDL);
 //   warp 1      TMEM allocator and MMA issuer (one elected lane);
 //   warp 2      B producer: 1-D bulk copies of the plane tiles (after PDL wait);
-//   warps 3..10 converters: thread = weight row; read the row's words from
-//               the swizzled SMEM tile, build A, tcgen05.st it into the TMEM A
-//               ring (software-pipelined: a slot is published while the next
-//               is built); warps 3..6 also run the epilogue.
+//   warps 3..10 converters: thread = weight row; read the row's words of the
+//               pass's one or two tiles from the swizzled SMEM ring, build A,
+//               tcgen05.st it into the TMEM A ring (software-pipelined: a slot
+//               is published while the next is built); warps 3..6 also run
+//               the epilogue.
 #include <cuda.h>
 #include <cstdint>
 #include <cstdio>
@@ -142,15 +147,53 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// 8 packed words -> 32 nibble registers (see the file header)
-__device__ __forceinline__ void build_a(const uint4 w0, const uint4 w1, uint32_t (&v)[32]) {
-    const uint32_t ws[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+// 8 words of the hi layer and 8 of the lo layer -> 32 nibble registers (file
+// header).  MODE 0: pair; 1: pair, hi = sign layer (complemented); 2: lo alone
+// (hi = 0); 3: lo alone and it is the sign layer (complemented).
+template <int MODE>
+__device__ __forceinline__ void build_a(const uint4 h0, const uint4 h1, const uint4 l0, const uint4 l1,
+                                        uint32_t (&v)[32]) {
+    const uint32_t hs[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+    const uint32_t ls[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
 #pragma unroll
     for (int uu = 0; uu < 8; ++uu) {
-        v[uu * 4 + 0] = ws[uu] & 0x11111111u;
-        v[uu * 4 + 1] = ws[uu] & 0x22222222u;
-        v[uu * 4 + 2] = ws[uu] & 0x44444444u;
-        v[uu * 4 + 3] = (ws[uu] >> 1) & 0x44444444u;
+        const uint32_t lo = (MODE == 3) ? ~ls[uu] : ls[uu];
+        if (MODE >= 2) {
+            v[uu * 4 + 0] = lo & 0x11111111u;
+            v[uu * 4 + 1] = (lo >> 1) & 0x11111111u;
+            v[uu * 4 + 2] = (lo >> 2) & 0x11111111u;
+            v[uu * 4 + 3] = (lo >> 3) & 0x11111111u;
+        } else {
+            const uint32_t hi = (MODE == 1) ? ~hs[uu] : hs[uu];
+            v[uu * 4 + 0] = ((hi << 1) & 0x22222222u) | (lo & 0x11111111u);
+            v[uu * 4 + 1] = (hi & 0x22222222u) | ((lo >> 1) & 0x11111111u);
+            v[uu * 4 + 2] = ((hi >> 1) & 0x22222222u) | ((lo >> 2) & 0x11111111u);
+            v[uu * 4 + 3] = ((hi >> 2) & 0x22222222u) | ((lo >> 3) & 0x11111111u);
+        }
+    }
+}
+
+// One pass of one row: 4 x (8 hi + 8 lo words from the swizzled SMEM tiles ->
+// 32 A registers -> tcgen05.st of 32 TMEM columns).
+template <int MODE>
+__device__ __forceinline__ void convert_pass(uint32_t thi, uint32_t tlo, uint32_t swz, uint32_t dst, int dbg) {
+#pragma unroll 1
+    for (int b4 = 0; b4 < 4; ++b4) {
+        // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
+        const uint32_t c0 = (((uint32_t)(2 * b4)) ^ swz) << 4;
+        const uint32_t c1 = (((uint32_t)(2 * b4 + 1)) ^ swz) << 4;
+        const uint4 l0 = lds128(tlo + c0), l1 = lds128(tlo + c1);
+        uint4 h0 = l0, h1 = l1;
+        if (MODE <= 1) {
+            h0 = lds128(thi + c0);
+            h1 = lds128(thi + c1);
+        }
+        uint32_t v[32];
+        build_a<MODE>(h0, h1, l0, l1, v);
+        if (dbg != 1 && dbg != 3)
+            st_tmem_x32(dst + (uint32_t)(32 * b4), v);
+        else if (v[0] == 0x12345 && v[3] == 0x777)
+            asm volatile("trap;");   // keep the ALU work alive
     }
 }
 
@@ -169,35 +212,38 @@ __device__ __forceinline__ void build_a(const uint4 w0, const uint4 w1, uint32_t
 // Host-chosen decomposition and TMEM map: [0, 128*slots) A ring,
 // [sf_col, sf_col + 64): columns 0..3 = SFA (1.0), columns 4(1+s).. = SFB 2^s
 // (scale-factor operands are addressed at 4-column granularity);
-// [d_col, d_col + regions*NPAD): accumulators (region 0 = sign layer).
+// [d_col, d_col + regions*NPAD): one accumulator per group of passes.
 struct TcPlan {
     int tiles;        // ceil(R / 128)
     int chunks;       // 32-word K-chunks per tile
     long long units;  // tiles * chunks
     int slots, sf_col, d_col;
-    int G;            // magnitude layers per accumulator group (K * 2^G < 2^24)
-    int regions;      // 1 + ceil((k_used - 1) / G)
+    int passes;       // ceil(k_used / 2): layer pairs (0,1), (2,3), ...
+    int Gp;           // passes per accumulator group (<= G/2 layers pairs, K * 2^G <= 2^24)
+    int regions;      // ceil(passes / Gp)
     int dbg;          // profiling knob (env PB_TC_DEBUG): 1 = no A store, 2 = no MMA, 3 = neither,
                       // 6 = per-CTA timeline
     int prof;         // env PB_TC_PROF: print wait-cycle totals of CTA 0
 };
 
-// Accumulator region of layer i, its block-scale exponent s (weight 2^s inside
-// the region) and whether i opens its region (first MMA overwrites).
-__device__ __forceinline__ void layer_region(const TcPlan& p, int k_used, int i, int& region, int& s, bool& first) {
-    if (i == 0) {
-        region = 0;
-        s = 0;
-        first = true;
-        return;
-    }
-    const int gi = (i - 1) / p.G;
-    const int lo = 1 + gi * p.G;                  // first (most significant) layer of the group
-    int hi = lo + p.G - 1;                        // last layer of the group
-    if (hi > k_used - 1) hi = k_used - 1;
-    region = 1 + gi;
-    s = hi - i;
-    first = (i == lo);
+// Least significant layer of pass ps (the pass's unit weight is |S_lo|).
+__device__ __host__ __forceinline__ int pass_lo(int k_used, int ps) {
+    return (2 * ps + 1 < k_used) ? 2 * ps + 1 : 2 * ps;
+}
+// Accumulator region of pass ps, its block-scale exponent s (weight 2^s
+// relative to the region's least significant layer) and whether it opens
+// the region (first MMA overwrites).
+__device__ __forceinline__ void pass_region(const TcPlan& p, int k_used, int ps, int& region, int& s, bool& first) {
+    region = ps / p.Gp;
+    int last = (region + 1) * p.Gp - 1;
+    if (last > p.passes - 1) last = p.passes - 1;
+    s = pass_lo(k_used, last) - pass_lo(k_used, ps);
+    first = (ps == region * p.Gp);
+}
+// |S_i|: 2^(L-1-i); the binary layer (offset 1) has |S_0| = 2.
+__device__ __forceinline__ unsigned long long layer_mag(int L, int offset, int i) {
+    if (i == 0 && offset) return 2ull;
+    return 1ull << (L - 1 - i);
 }
 
 // A CTA's units [u0, u1) split into segments of one row tile: [kcA, kcB) of tile rt.
@@ -344,10 +390,10 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 TWAIT(&bars.b_full[st], (uint32_t)((cc >> 1) & 1), 1);
                 tc_fence_after();
                 const uint64_t bdesc0 = b_desc(smem_u32(btile0 + st * kBStage));
-                for (int i = 0; i < g.k_used; ++i) {
+                for (int ps = 0; ps < p.passes; ++ps) {
                     int region, sexp;
                     bool first;
-                    layer_region(p, g.k_used, i, region, sexp, first);
+                    pass_region(p, g.k_used, ps, region, sexp, first);
                     const uint32_t dcol = tmem + (uint32_t)(p.d_col + region * NPAD);
                     const uint32_t sfb = tmem + (uint32_t)(p.sf_col + 4 * (1 + sexp));
                     const bool open = first && kc == sg.kcA;
@@ -386,11 +432,11 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const uint32_t wtile_s = smem_u32(wtile0) + (uint32_t)m * 128;
         const uint32_t swz = (uint32_t)(m & 7);
-        int tc = 0, seg = 0;
-        // tiles (kc, i) in issue order; h-set h converts tiles t = h, h + 2, ...; tile t uses
-        // A slot t % slots
+        int tc = 0, pc = 0, seg = 0;
+        // passes (kc, ps) in issue order; h-set h converts passes pc = h, h + 2, ...; pass pc
+        // uses A slot pc % slots; its tiles are tc (hi, if paired) and tc + 1 (or tc alone)
         int slot = h % p.slots, sphase = (h / p.slots) & 1;
-        // software pipeline: the TMEM stores of one tile drain while the next is awaited
+        // software pipeline: the TMEM stores of one pass drain while the next is awaited
         int pend_slot = -1;
         auto publish = [&]() {
             if (pend_slot >= 0) {
@@ -406,30 +452,36 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             const int64_t row = (int64_t)sg.rt * kTcRows + m;
             const bool row_ok = row < g.R;
             for (int kc = sg.kcA; kc < sg.kcB; ++kc) {
-                for (int i = 0; i < g.k_used; ++i, ++tc) {
-                    if ((tc & 1) != h) continue;
-                    const int st = tc % kWStages;
-                    TWAIT(&bars.w_full[st], (uint32_t)((tc / kWStages) & 1), 3);
-                    const uint32_t trow = wtile_s + (uint32_t)st * kWTileBytes;
-                    publish();                          // previous tile's A is in TMEM: tell the MMA
+                for (int ps = 0; ps < p.passes; ++ps, ++pc) {
+                    const bool paired = 2 * ps + 1 < g.k_used;
+                    const int ntile = paired ? 2 : 1;
+                    if ((pc & 1) != h) {
+                        tc += ntile;
+                        continue;
+                    }
+                    const int st_hi = tc % kWStages, st_lo = (tc + ntile - 1) % kWStages;
+                    TWAIT(&bars.w_full[st_hi], (uint32_t)((tc / kWStages) & 1), 3);
+                    if (paired)
+                        TWAIT(&bars.w_full[st_lo], (uint32_t)(((tc + 1) / kWStages) & 1), 3);
+                    const uint32_t thi = wtile_s + (uint32_t)st_hi * kWTileBytes;
+                    const uint32_t tlo = wtile_s + (uint32_t)st_lo * kWTileBytes;
+                    publish();                          // previous pass's A is in TMEM: tell the MMA
                     TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
                     tc_fence_after();
-                    if (p.dbg != 7) {
-#pragma unroll 1
-                        for (int b4 = 0; b4 < 4; ++b4) {
-                            // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
-                            const uint4 w0 = lds128(trow + ((((uint32_t)(2 * b4)) ^ swz) << 4));
-                            const uint4 w1 = lds128(trow + ((((uint32_t)(2 * b4 + 1)) ^ swz) << 4));
-                            uint32_t v[32];
-                            build_a(w0, w1, v);
-                            if (p.dbg != 1 && p.dbg != 3)
-                                st_tmem_x32(tmem + lane_off + (uint32_t)(slot * 128 + 32 * b4), v);
-                            else if (v[0] == 0x12345 && v[3] == 0x777)
-                                asm volatile("trap;");   // keep the ALU work alive
-                        }
+                    const int mode = paired ? (ps == 0 ? 1 : 0) : (ps == 0 ? 3 : 2);
+                    const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
+                    switch (mode) {
+                        case 0: convert_pass<0>(thi, tlo, swz, dst, p.dbg); break;
+                        case 1: convert_pass<1>(thi, tlo, swz, dst, p.dbg); break;
+                        case 2: convert_pass<2>(thi, tlo, swz, dst, p.dbg); break;
+                        default: convert_pass<3>(thi, tlo, swz, dst, p.dbg); break;
                     }
                     __syncwarp();                       // this warp's words are in TMEM-bound registers
-                    if (lane == 0) mbar_arrive(&bars.w_empty[st]);
+                    if (lane == 0) {
+                        mbar_arrive(&bars.w_empty[st_hi]);
+                        if (paired) mbar_arrive(&bars.w_empty[st_lo]);
+                    }
+                    tc += ntile;
                     pend_slot = slot;
                     slot += 2;
                     while (slot >= p.slots) {
@@ -445,16 +497,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 mbar_wait(&bars.d_full, (uint32_t)(seg & 1));
                 tc_fence_after();
                 pdl_wait();
-                // tot_b = sum_j T_j sum_r w_r D_r[b*a + j]; region weights: S_0 for the sign
-                // layer, S_hi (its least significant layer) for a magnitude group
+                // tot_b = sum_j T_j sum_r |S_lo(r)| D_r[b*a + j] (+ the sign correction below);
+                // lo(r) = least significant layer of group r
                 for (int b = 0; b < g.B; ++b) s_tot[b * kTcRows + m] = 0;
                 for (int r = 0; r < p.regions; ++r) {
-                    int hi = 0;
-                    if (r > 0) {
-                        hi = r * p.G;
-                        if (hi > g.k_used - 1) hi = g.k_used - 1;
-                    }
-                    const unsigned long long wr = layer_scale(g.L, g.offset, hi);
+                    int last = (r + 1) * p.Gp - 1;
+                    if (last > p.passes - 1) last = p.passes - 1;
+                    const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
 #pragma unroll 1
                     for (int c = 0; c < NPAD; c += 8) {
                         uint32_t t8[8];
@@ -514,11 +563,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                                 t += __ldcg(g.slots + (((int64_t)c * 2 + sslot) * g.B + b) * kTcRows + m);
                             }
                         }
-                        if (g.offset) {
+                        {
+                            // (o - |S_0|) * sum_c x_q: the binary offset (o = 1) and the
+                            // complemented sign layer (file header)
                             unsigned long long sx = 0;
                             for (int pp = 0; pp < g.nsplit; ++pp)
                                 sx += (unsigned long long)g.xsum[(int64_t)b * kMaxSplit + pp];
-                            t += (unsigned long long)g.offset * sx;
+                            t += ((unsigned long long)g.offset - layer_mag(g.L, g.offset, 0)) * sx;
                         }
                         const long long accv = (long long)t;
                         const int64_t o = (int64_t)b * g.R + row;
@@ -591,11 +642,13 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     if (p.tiles > kMaxTiles) return false;
     p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
     p.units = (long long)p.tiles * p.chunks;
-    // exact f32 accumulation: a group sum is < K * 2^G <= 2^24
-    p.G = 24 - ceil_log2_i(g.kwords * 32);
-    if (p.G > 15) p.G = 15;                       // 15 SFB scale values fit the 64-column SF area
-    if (p.G < 1) return false;
-    p.regions = 1 + (g.k_used - 1 + p.G - 1) / p.G;
+    // exact f32 accumulation: a group of G layers sums to < K * 2^G <= 2^24
+    int G = 24 - ceil_log2_i(g.kwords * 32);
+    if (G > 15) G = 15;                           // SFB exponents 0..13 fit the 64-column SF area
+    p.Gp = G / 2;
+    if (p.Gp < 1) return false;
+    p.passes = (g.k_used + 1) / 2;
+    p.regions = (p.passes + p.Gp - 1) / p.Gp;
     if (p.regions > kMaxRegions) return false;
     p.d_col = 512 - (p.regions * npad + 31) / 32 * 32;
     p.sf_col = p.d_col - 64;
