@@ -23,6 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-I", INC, "-I", CSRC, "-Xcompiler", "-fPIC,-fopenmp"]
+# experiment knobs only (e.g. PB_NVCC_DEFS="-DPB_CONV_UNROLL=2"); the shipped build uses none
+COMMON += os.environ.get("PB_NVCC_DEFS", "").split()
 
 
 def _headers():

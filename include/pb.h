@@ -63,11 +63,19 @@ enum { PB_ENGINE_AUTO = 0, PB_ENGINE_POPC = 1, PB_ENGINE_MMA = 2 };
 
 /*
  * Packed weight bitlayers (D1).  Plain descriptor; `bits` is
- * caller-owned memory (host or device) holding
- *     bits[layer][row][kwords]   uint32 words, 16-byte aligned rows,
- * layer 0 = the sign layer, layer i holds bit (L-1-i) of the
- * L-bit two's-complement code; bit j of word w <-> column 32*w + j; padding
- * columns are zero (AND-neutral).  kwords = 4*ceil(cols/128).
+ * caller-owned memory (host or device) of L * rows * kwords uint32 words.
+ * Bitlayer W_i: layer 0 = the sign layer, layer i holds bit
+ * (L-1-i) of the L-bit two's-complement code; padding columns are zero
+ * (AND-neutral).  kwords = 4*ceil(cols/128).  Its canonical word for
+ * 32-column block c of row r is  Wc_i[r][c] = sum_j W_i[r, 32c + j] << j.
+ * Storage ("paired bitlayers", the stacking of P:206): layers (2p, 2p+1)
+ * share the span of layer slots 2p and 2p+1, as rows of 2*kwords words
+ *     pair[p][row][2c + e],  e = 0 (even columns), 1 (odd columns),
+ *     bit 2k   of pair[p][r][2c + e] = W_{2p+1}[r, 32c + 2k + e]   (lower)
+ *     bit 2k+1 of pair[p][r][2c + e] = W_{2p}  [r, 32c + 2k + e]   (upper)
+ * so each 2-bit field is one column's (upper, lower) bit pair.  With L odd
+ * the last layer W_{L-1} is stored canonically in slot L-1:
+ *     bits[(L-1)*rows*kwords + r*kwords + c] = Wc_{L-1}[r][c].
  * Represented weight: W ~= scale * (sum_i S_i * W_i + offset) with
  * S_0 = -2^(L-1) (or -2 when offset = 1, binary mode) and S_i = 2^(L-1-i).
  */
@@ -132,8 +140,10 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
 /*
  * Workspace of one call (batch columns of a layer with `cols` inputs):
  *   [stream-K tile counters int32 x 8192]     zero on entry, left zero on exit
+ *   [grid barrier int32 x 2]                  arrival count (zero on entry,
+ *                                             left zero) + generation
  *   [tensor-engine partial-tile slots int64 x 160 x 2 x batch x 128]
- *   [f_b int32 x batch][x_q partial sums int64 x batch x 64]
+ *   [f_b int32 x batch][x_q partial sums int64 x batch x 160]
  *   [planes uint32 x batch x act_bits x kwords]
  *   [tensor-engine B operand tiles: kwords x N_pad x 32 bytes, N_pad = a*batch
  *    padded to 8/16/32, present when a*batch <= 32]
@@ -206,6 +216,18 @@ pb_status pb_lstm_step(const float* x_t, const float* h, const float* c,
 /* Select the binary-product engine (process-wide; default AUTO). */
 pb_status pb_set_engine(int32_t engine);
 int32_t pb_get_engine(void);
+
+/* Diagnostics: per-CTA kernel timeline (globaltimer ns), kept only when the
+ * environment variable PB_TC_DEBUG=6 is set at the library's first launch.
+ * Copies up to max_records records of 10 int64 each into host memory dst:
+ *   {kind, cta, sm, units, t0, t1, t2, t3, t4, t5}
+ *   kind 0 = activation cast/transpose CTA: t0 launch, t1 PDL wait done, t2 end;
+ *   kind 1 = tensor-engine GEMM CTA: t0 start, t1 B operand ready (PDL wait
+ *            done), t2 first MMA issue, t3 last MMA issue, t4 epilogue done,
+ *            t5 exit.
+ * Synchronises the device, clears the log and returns the number of records
+ * copied; -1 when no log is kept. */
+int64_t pb_debug_timeline(int64_t* dst, int64_t max_records);
 
 /* ---------------- multi-GPU row sharding ----------------
  * Rank g of N holds rows [row0, row0 + nrows) of every bitlayer, packed as

@@ -44,6 +44,7 @@ _W = C.POINTER(pb_weights)
 _SIGS = {
     "pb_last_error": ([], C.c_char_p),
     "pb_version": ([], C.c_char_p),
+    "pb_debug_timeline": ([_p, _i64], _i64),
     "pb_kwords": ([_i64], _i64),
     "pb_packed_bytes": ([_i64, _i64, _i32], _sz),
     "pb_quantize_pack_weights": ([_p, _i64, _i64, _i32, _i32, _f32, _p, _i32, _p, _W], _i32),
@@ -329,3 +330,11 @@ def shard_grid_step(W_min, W_max, L):
     if d == 0.0:
         d = abs(float(W_max)) or 1.0
     return d
+
+
+def debug_timeline(max_records=1 << 16):
+    """Per-CTA kernel timeline records (pb_debug_timeline; PB_TC_DEBUG=6), as an
+    int64 array [n][10], or None when no log is kept."""
+    buf = np.zeros((max_records, 10), np.int64)
+    n = _lib.pb_debug_timeline(buf.ctypes.data, max_records)
+    return None if n < 0 else buf[:n]

@@ -19,6 +19,8 @@
 // (an L2-resident re-read of K floats) so no second launch or grid sync is
 // needed; it then transposes its own slice of words.
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "pb_common.cuh"
@@ -35,9 +37,12 @@ __global__ void __launch_bounds__(kThreads)
 act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kwords, int a,
                            int act_frac, int words_per_cta, int32_t* __restrict__ f_out,
                            long long* __restrict__ xsum_part, uint32_t* __restrict__ planes,
-                           uint8_t* __restrict__ bexp, int npad)
+                           uint8_t* __restrict__ bexp, int npad, long long* tl)
 {
+    long long t_launch = 0, t_go = 0;
+    if (tl) t_launch = gtimer();
     pdl_wait();          // x may be the previous kernel's output
+    if (tl) t_go = gtimer();
     pdl_trigger();       // let the dependent GEMV start its prologue
 
     const int b = blockIdx.y;
@@ -74,22 +79,10 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
 #pragma unroll
     for (int w = 1; w < kWarps; ++w) m = fmaxf(m, s_max[w]);
 
-    int f;
-    if (act_frac == kActAuto) {
-        if (m == 0.f) {
-            f = 0;
-        } else {
-            int e;
-            frexpf(m, &e);           // m = frac * 2^e, frac in [0.5, 1): m < 2^e
-            f = (a - 1) - e;
-        }
-    } else {
-        f = act_frac;
-    }
+    const int f = (act_frac == kActAuto) ? act_frac_of(m, a) : act_frac;
     if (blockIdx.x == 0 && tid == 0) f_out[b] = f;
 
     // ---- a1 (part 2) + a2: cast, saturate, ballot-transpose ----
-    const double lo = -ldexp(1.0, a - 1), hi = ldexp(1.0, a - 1) - 1.0;
     const int64_t w0 = (int64_t)blockIdx.x * words_per_cta;
     int64_t w1 = w0 + words_per_cta;
     if (w1 > kwords) w1 = kwords;
@@ -99,9 +92,7 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
     for (int64_t w = w0 + warp; w < w1; w += kWarps) {
         const int64_t c = 32 * w + lane;
         const float v = c < K ? __ldg(xb + c) : 0.f;
-        double t = ldexp((double)v, f);          // exact power-of-two scaling
-        t = fmin(fmax(t, lo), hi);               // saturation (literal act_frac only)
-        const long long q = __double2ll_rz(t);   // Int() = truncation toward zero
+        const long long q = act_cast(v, f, a);
         xs += q;
         uint32_t mine = 0;
         for (int j = 0; j < a; ++j) {
@@ -110,19 +101,10 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
         }
         if (lane < a && w < kwords) pb[(int64_t)lane * kwords + w] = mine;
         if (npad) {
-            // tile (w / 2), k-half (w % 2); lane j < a writes plane row n = b*a + j
-            uint8_t* tile = bexp + (int64_t)(w >> 1) * npad * 32 + (w & 1) * 128;
-            const uint32_t p = mine;
-            auto put = [&](int n, uint4 v) {
-                *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + (n & 7) * 16) = v;
-            };
-            if (lane < a)
-                put(b * a + lane, make_uint4(((p >> 0) & 0x11111111u) << 2, ((p >> 1) & 0x11111111u) << 2,
-                                             ((p >> 2) & 0x11111111u) << 2, ((p >> 3) & 0x11111111u) << 2));
-            if (b == (int)gridDim.y - 1) {   // zero padding rows n in [a*B, npad)
-                const int n = (int)gridDim.y * a + lane;
-                if (n < npad) put(n, make_uint4(0u, 0u, 0u, 0u));
-            }
+            // lane j < a writes plane row n = b*a + j; the last batch column zeroes rows [a*B, npad)
+            if (lane < a) put_b_operand(bexp, npad, w, b * a + lane, mine);
+            if (b == (int)gridDim.y - 1 && (int)gridDim.y * a + lane < npad)
+                put_b_operand(bexp, npad, w, (int)gridDim.y * a + lane, 0u);
         }
     }
 #pragma unroll
@@ -132,11 +114,37 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
     if (tid == 0) {
         long long t = 0;
         for (int w = 0; w < kWarps; ++w) t += s_sum[w];
-        xsum_part[(int64_t)b * kMaxSplit + blockIdx.x] = t;
+        xsum_part[(int64_t)b * kXsumStride + blockIdx.x] = t;
+        if (tl) {
+            long long* r = tl_record(tl);
+            if (r) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                const long long rec[10] = {0, blockIdx.x + (long long)blockIdx.y * gridDim.x, smid, 0, t_launch, t_go,
+                                           gtimer(), 0, 0, 0};
+                for (int k = 0; k < 10; ++k) r[k] = rec[k];
+            }
+        }
     }
 }
 
 }  // namespace
+
+// Diagnostics timeline buffer (pb_debug_timeline): allocated at the first
+// launch when PB_TC_DEBUG=6, else null.
+long long* debug_tl() {
+    static int state = 0;          // 0 = unknown, 1 = off, 2 = on
+    static long long* buf = nullptr;
+    if (state == 0) {
+        const char* ev = getenv("PB_TC_DEBUG");
+        state = 1;
+        if (ev && atoi(ev) == 6 &&
+            cudaMalloc(&buf, sizeof(long long) * (size_t)(10 + 10 * kTlRecords)) == cudaSuccess &&
+            cudaMemset(buf, 0, sizeof(long long) * 10) == cudaSuccess)
+            state = 2;
+    }
+    return state == 2 ? buf : nullptr;
+}
 
 cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kwords, int a,
                              int act_frac, void* ws, const WsLayout& l, cudaStream_t s)
@@ -167,7 +175,7 @@ cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kword
                               reinterpret_cast<int32_t*>(base + l.off_f),
                               reinterpret_cast<long long*>(base + l.off_xsum),
                               reinterpret_cast<uint32_t*>(base + l.off_planes),
-                              reinterpret_cast<uint8_t*>(base + l.off_bexp), l.npad);
+                              reinterpret_cast<uint8_t*>(base + l.off_bexp), l.npad, debug_tl());
 }
 
 }  // namespace pb

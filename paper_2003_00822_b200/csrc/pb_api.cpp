@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -188,6 +189,28 @@ pb_status pack(const int32_t* codes, int64_t R, int64_t K, int L, int offset, st
     }
     if (bad) return fail(PB_ERANGE, "a code does not fit %d-bit two's complement%s", L,
                          offset ? " (binary mode needs codes +-1)" : "");
+    // paired storage (pb.h): layers (2p, 2p+1) -> rows of 2*kw words, even/odd columns
+    // interleaved as (lower, upper) bit pairs; an odd last layer stays canonical
+    if (L >= 2) {
+        const std::vector<uint32_t> canon(out.begin(), out.begin() + (size_t)(L / 2) * 2 * R * kw);
+        for (int p = 0; 2 * p + 1 < L; ++p) {
+#pragma omp parallel for schedule(static)
+            for (int64_t r = 0; r < R; ++r) {
+                const uint32_t* hi = &canon[((size_t)(2 * p) * R + r) * kw];
+                const uint32_t* lo = &canon[((size_t)(2 * p + 1) * R + r) * kw];
+                uint32_t* dst = &out[(size_t)(2 * p) * R * kw + (size_t)r * 2 * kw];
+                for (int64_t c = 0; c < kw; ++c) {
+                    uint32_t e0 = 0, e1 = 0;
+                    for (int k = 0; k < 16; ++k) {
+                        e0 |= ((lo[c] >> (2 * k)) & 1u) << (2 * k) | ((hi[c] >> (2 * k)) & 1u) << (2 * k + 1);
+                        e1 |= ((lo[c] >> (2 * k + 1)) & 1u) << (2 * k) | ((hi[c] >> (2 * k + 1)) & 1u) << (2 * k + 1);
+                    }
+                    dst[2 * c] = e0;
+                    dst[2 * c + 1] = e1;
+                }
+            }
+        }
+    }
     return PB_OK;
 }
 
@@ -410,13 +433,13 @@ static pb_status validate_gemm(const void* ws, size_t ws_bytes, int64_t batch, c
     return PB_OK;
 }
 
-pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_weights* w, int32_t k_used,
-                     int32_t act_bits, float* y, int64_t* acc, const float* bias, int32_t fn,
-                     int32_t accumulate, pb_stream s) {
-    g_err[0] = 0;
-    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, fn);
-    if (st != PB_OK) return st;
-    if (batch == 0 || w->rows == 0) return PB_OK;
+// Steps a3-a5 (and, when x is given and the tensor engine takes the shape, a1-a2
+// fused into the same kernel).  Returns PB_EINVAL with *fused_done = false when x
+// is given but the fused path does not apply (the caller then runs a1-a2 first).
+static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
+                          float* y, int64_t* acc, const float* bias, int32_t fn, int32_t accumulate, pb_stream s,
+                          const float* x, int32_t act_frac, bool* fused_done) {
+    if (fused_done) *fused_done = false;
 
     const pb::WsLayout l = pb::ws_layout(batch, w->kwords, act_bits);
     char* base = static_cast<char*>(const_cast<void*>(ws));
@@ -430,8 +453,8 @@ pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_we
     g.a = act_bits;
     g.scale = w->scale;
     g.planes = reinterpret_cast<const uint32_t*>(base + l.off_planes);
-    g.f = reinterpret_cast<const int32_t*>(base + l.off_f);
-    g.xsum = reinterpret_cast<const long long*>(base + l.off_xsum);
+    g.f = reinterpret_cast<int32_t*>(base + l.off_f);
+    g.xsum = reinterpret_cast<long long*>(base + l.off_xsum);
     g.nsplit = pb::act_nsplit(w->kwords);
     g.B = batch;
     g.y = y;
@@ -440,12 +463,25 @@ pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_we
     g.fn = fn;
     g.accumulate = accumulate ? 1 : 0;
     g.npad = l.npad;
-    g.bexp = reinterpret_cast<const uint8_t*>(base + l.off_bexp);
+    g.bexp = reinterpret_cast<uint8_t*>(base + l.off_bexp);
     g.slots = reinterpret_cast<unsigned long long*>(base + l.off_slots);
     g.counters = reinterpret_cast<int*>(base + l.off_count);
+    g.tl = pb::debug_tl();
+    g.x = nullptr;
+    g.K = w->cols;
+    g.act_frac = act_frac;
+    g.gbar = g.counters + pb::kMaxTiles;
 
     cudaError_t e;
     const cudaStream_t cs = static_cast<cudaStream_t>(s);
+    if (x) {
+        if (g_engine == PB_ENGINE_POPC || !pb::tc_supported(g)) return PB_EINVAL;
+        g.x = x;
+        e = pb::launch_gemm_tc(g, cs);
+        if (e != cudaSuccess) return cuda_fail(e, "fused bitgemm launch");
+        *fused_done = true;
+        return PB_OK;
+    }
     if (g_engine == PB_ENGINE_MMA) {
         if (!pb::tc_supported(g))
             return fail(PB_EINVAL, "PB_ENGINE_MMA needs act_bits*batch <= 32 and k_used*N_pad <= 256");
@@ -459,25 +495,44 @@ pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_we
     return PB_OK;
 }
 
+pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_weights* w, int32_t k_used,
+                     int32_t act_bits, float* y, int64_t* acc, const float* bias, int32_t fn,
+                     int32_t accumulate, pb_stream s) {
+    g_err[0] = 0;
+    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, fn);
+    if (st != PB_OK) return st;
+    if (batch == 0 || w->rows == 0) return PB_OK;
+    return run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, accumulate, s, nullptr, 0, nullptr);
+}
+
+// a1-a5: one fused tensor-engine kernel when it takes the shape, else the
+// activation kernel followed by pb_bitgemm's engine.
+static pb_status act_and_gemm(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
+                              int32_t act_frac, const float* bias, int32_t fn, float* y, int64_t* acc, void* ws,
+                              size_t ws_bytes, pb_stream s) {
+    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, fn);
+    if (st != PB_OK) return st;
+    if ((st = check_act(batch, w->cols, act_bits, act_frac)) != PB_OK) return st;
+    if (batch == 0 || w->rows == 0) return PB_OK;
+    if (!x || !aligned(x, 4)) return fail(PB_EINVAL, "x must be a non-NULL device pointer");
+    bool fused = false;
+    st = run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, x, act_frac, &fused);
+    if (fused || (st != PB_OK && st != PB_EINVAL)) return st;
+    if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
+    return run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, nullptr, 0, nullptr);
+}
+
 pb_status pb_matmul(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
                     int32_t act_frac, float* y, int64_t* acc, void* ws, size_t ws_bytes, pb_stream s) {
     g_err[0] = 0;
-    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, PB_FN_NONE);
-    if (st != PB_OK) return st;
-    if ((st = check_act(batch, w->cols, act_bits, act_frac)) != PB_OK) return st;
-    if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
-    return pb_bitgemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, nullptr, PB_FN_NONE, 0, s);
+    return act_and_gemm(x, batch, w, k_used, act_bits, act_frac, nullptr, PB_FN_NONE, y, acc, ws, ws_bytes, s);
 }
 
 pb_status pb_linear(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
                     int32_t act_frac, const float* bias, int32_t fn, float* y, void* ws, size_t ws_bytes,
                     pb_stream s) {
     g_err[0] = 0;
-    pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, nullptr, fn);
-    if (st != PB_OK) return st;
-    if ((st = check_act(batch, w->cols, act_bits, act_frac)) != PB_OK) return st;
-    if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
-    return pb_bitgemm(ws, ws_bytes, batch, w, k_used, act_bits, y, nullptr, bias, fn, 0, s);
+    return act_and_gemm(x, batch, w, k_used, act_bits, act_frac, bias, fn, y, nullptr, ws, ws_bytes, s);
 }
 
 size_t pb_cell_workspace_bytes(int64_t batch, int64_t in_cols, int64_t hidden, int32_t act_bits, int32_t gates) {
@@ -542,6 +597,24 @@ pb_status pb_set_engine(int32_t engine) {
     return PB_OK;
 }
 int32_t pb_get_engine(void) { return g_engine; }
+
+// ------------------------------------------------------------ diagnostics timeline
+
+int64_t pb_debug_timeline(int64_t* dst, int64_t max_records) {
+    long long* tl = pb::debug_tl();
+    if (!tl) return -1;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
+    long long n = 0;
+    if (cudaMemcpy(&n, tl, sizeof n, cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    if (n > pb::kTlRecords) n = pb::kTlRecords;
+    if (n > max_records) n = max_records;
+    if (n > 0 && dst &&
+        cudaMemcpy(dst, tl + 10, sizeof(long long) * 10 * (size_t)n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -1;
+    cudaMemset(tl, 0, sizeof(long long));
+    cudaDeviceSynchronize();
+    return n;
+}
 
 // ------------------------------------------------------------ row sharding
 pb_status pb_shard_rows(int64_t rows_total, int32_t nranks, int32_t rank, int64_t* row0, int64_t* nrows) {

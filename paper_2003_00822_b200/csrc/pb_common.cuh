@@ -3,6 +3,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "pb_internal.h"
+
 namespace pb {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -56,6 +58,48 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // Shift-weighted reduction scales: T_j and S_i as wrapping
 // 64-bit integers.  All accumulation is done modulo 2^64, which is exact as
 // long as the final value fits int64 (the G11 guard checked on the host).
+// Step a1 (Alg. 2 line 1; readings G7/G8): x_q = Int(x * 2^f) with
+// the power-of-two scaling exact in double, saturation to the a-bit two's
+// complement range (only reachable with a literal act_frac) and truncation
+// toward zero.
+__device__ __forceinline__ double pow2d(int e) {   // 2^e, e in [-1022, 1023]
+    return __hiloint2double((1023 + e) << 20, 0);
+}
+__device__ __forceinline__ long long act_cast(float v, int f, int a) {
+    const double lim = (double)(1ll << (a - 1));
+    double t = (f >= -1000 && f <= 1000) ? (double)v * pow2d(f) : ldexp((double)v, f);
+    t = fmin(fmax(t, -lim), lim - 1.0);
+    return __double2ll_rz(t);
+}
+// f_b from max|x[b,:]| (reading G8): the largest f with max|x| * 2^f < 2^(a-1).
+__device__ __forceinline__ int act_frac_of(float m, int a) {
+    if (m == 0.f) return 0;
+    int e;
+    frexpf(m, &e);           // m = frac * 2^e, frac in [0.5, 1): m < 2^e
+    return (a - 1) - e;
+}
+// Tensor-engine B operand (pb_gemm_tc.cu): plane word p of plane row n for
+// word w, as 4 uint32 of e2m1 nibbles (X bit (4e + r) -> 2.0 = 0b0100) in the
+// K-major no-swizzle canonical layout of the N_pad x 32-byte tile of words
+// (w & ~1, w | 1).
+__device__ __forceinline__ void put_b_operand(uint8_t* bexp, int npad, int64_t w, int n, uint32_t p) {
+    uint8_t* tile = bexp + (w >> 1) * npad * 32 + (w & 1) * 128;
+    *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + (n & 7) * 16) =
+        make_uint4((p & 0x11111111u) << 2, ((p >> 1) & 0x11111111u) << 2, ((p >> 2) & 0x11111111u) << 2,
+                   ((p >> 3) & 0x11111111u) << 2);
+}
+
+// Next diagnostics-timeline record (pb_internal.h, pb_debug_timeline) or null when full.
+__device__ __forceinline__ long long* tl_record(long long* tl) {
+    const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(tl), 1ull);
+    return i < (unsigned long long)kTlRecords ? tl + 10 + 10 * (long long)i : nullptr;
+}
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ unsigned long long plane_scale(int a, int j) {
     const unsigned long long p = 1ull << (a - 1 - j);
     return j == 0 ? (0ull - p) : p;

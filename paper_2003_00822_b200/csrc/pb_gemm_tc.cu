@@ -64,26 +64,41 @@ namespace pb {
 namespace {
 
 constexpr int kConvWarps = 8;                 // 2 h-sets of 4 warps (one per TMEM lane quarter)
-constexpr int kHSets = kConvWarps / 4;
 constexpr int kConv0 = 3;                     // first converter warp
 constexpr int kThreads = 32 * (kConv0 + kConvWarps);
 constexpr int kMaxSlots = 4;                  // A ring: up to 4 slots x 128 TMEM columns (16 MMAs each)
 constexpr int kMaxRegions = 4;                // TMEM accumulators: sign layer + magnitude groups
 constexpr int kChunkWords = 32;               // K-chunk = one 128-byte swizzle row
-constexpr int kWStages = 8;                   // weight tile ring
+constexpr int kActAutoFrac = -1024;           // == PB_ACT_AUTO
+#ifndef PB_MAX_WSTAGES
+#define PB_MAX_WSTAGES 16
+#endif
+#ifndef PB_PUBLISH_EARLY
+#define PB_PUBLISH_EARLY 1
+#endif
+constexpr int kMaxWStages = PB_MAX_WSTAGES;   // weight tile ring (stages sized per launch from free SMEM)
 constexpr uint32_t kWTileBytes = kTcRows * kChunkWords * 4;   // 16 KiB
-constexpr uint32_t kBStageMax = (kChunkWords / 2) * kTcMaxN * 32;   // 16 KiB
-constexpr uint32_t kTotBytes = kTcMaxN * kTcRows * 8;          // epilogue per-row, per-batch int64 sums
-constexpr uint32_t kSmemBytes = 1024 + 1024 + kWStages * kWTileBytes + 2 * kBStageMax + kTotBytes;
+constexpr uint32_t kSmemMax = 227 * 1024;                       // opt-in dynamic SMEM per CTA
+constexpr uint32_t kHdrBytes = 3072;                          // struct Bars
+// dynamic SMEM: [align slack][Bars][W ring: wstages x 16 KiB][B: 2 stages][s_tot: B x 128 int64]
 
 struct Bars {
     uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];   // a_full: the 4 warps of one h-set
-    uint64_t w_full[kWStages], w_empty[kWStages];
+    uint64_t w_full[kMaxWStages], w_empty[kMaxWStages];
     uint64_t b_full[2], b_empty[2];
     uint64_t d_full, d_empty;
+    uint64_t x_ready;                        // fused path: bars.xsum written (warp 2)
+    int gen;                                 // fused path: grid-barrier generation at arrival
     uint32_t tmem_base;
     int last_flag;
+    long long t_b, t_mma0, t_mend, t_cend;   // diagnostics timeline (globaltimer ns)
+    // fused activation prologue
+    float red[8 * kTcMaxN];                  // per-warp partial max|x[b,:]|
+    int f[kTcMaxN];                          // f_b
+    unsigned long long xs[kTcMaxN];          // this CTA's sum of x_q[b, slice]
+    unsigned long long xsum[kTcMaxN];        // sum_c x_q[b, c] over all CTAs
 };
+static_assert(sizeof(Bars) <= kHdrBytes, "Bars must fit the SMEM header");
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -144,52 +159,97 @@ __device__ __forceinline__ bool elect_one() {
         : "=r"(pred));
     return pred != 0;
 }
+template <int N>
+__device__ __forceinline__ void ld_tmem_cols(uint32_t addr, uint32_t (&v)[N]) {
+    static_assert(N % 8 == 0, "8-column granularity");
+#pragma unroll
+    for (int c = 0; c < N; c += 8) {
+        uint32_t t[8];
+        ld_tmem_x8(addr + c, t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[c + e] = t[e];
+    }
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// 8 words of the hi layer and 8 of the lo layer -> 32 nibble registers (file
-// header).  MODE 0: pair; 1: pair, hi = sign layer (complemented); 2: lo alone
-// (hi = 0); 3: lo alone and it is the sign layer (complemented).
+// A registers from the stored weights (pb.h), 8 32-column blocks -> 32
+// registers; register 4k + r holds in nibble e column 32k + 4e + r (the B
+// operand's order, pb_act.cu):
+//   paired storage: block k = words (P0, P1) = even / odd columns as
+//     (lower, upper) bit pairs, so nibble e of A_r is already the e2m1 code
+//     1.0*upper + 0.5*lower of column 4e + r after one mask (and a shift):
+//       A_0 = P0 & 0x33333333, A_1 = P1 & .., A_2 = (P0 >> 2) & .., A_3 = (P1 >> 2) & ..
+//     MODE 0 pair; 1 pair whose upper layer is the sign layer (complemented:
+//     P ^ 0xAAAAAAAA); 2 upper layer only (k_used odd: 0.5*upper, the pass
+//     unit becomes |S_upper|); 3 = 2 with the sign layer;
+//   canonical single layer (the last layer of an odd L): A_r = (w >> r) & 0x11111111,
+//     MODE 4; 5 = the complemented sign layer (L = 1).
 template <int MODE>
-__device__ __forceinline__ void build_a(const uint4 h0, const uint4 h1, const uint4 l0, const uint4 l1,
-                                        uint32_t (&v)[32]) {
-    const uint32_t hs[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-    const uint32_t ls[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+__device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t (&v)[32]) {
+    const uint32_t w[16] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w,
+                            q[2].x, q[2].y, q[2].z, q[2].w, q[3].x, q[3].y, q[3].z, q[3].w};
+    constexpr uint32_t kM3 = 0x33333333u, kM1 = 0x11111111u, kUp = 0xAAAAAAAAu;
 #pragma unroll
-    for (int uu = 0; uu < 8; ++uu) {
-        const uint32_t lo = (MODE == 3) ? ~ls[uu] : ls[uu];
-        if (MODE >= 2) {
-            v[uu * 4 + 0] = lo & 0x11111111u;
-            v[uu * 4 + 1] = (lo >> 1) & 0x11111111u;
-            v[uu * 4 + 2] = (lo >> 2) & 0x11111111u;
-            v[uu * 4 + 3] = (lo >> 3) & 0x11111111u;
+    for (int k = 0; k < 8; ++k) {
+        if (MODE <= 3) {
+            uint32_t p0 = w[2 * k], p1 = w[2 * k + 1];
+            if (MODE == 1 || MODE == 3) {
+                p0 ^= kUp;
+                p1 ^= kUp;
+            }
+            if (MODE <= 1) {
+                v[4 * k + 0] = p0 & kM3;
+                v[4 * k + 1] = p1 & kM3;
+                v[4 * k + 2] = (p0 >> 2) & kM3;
+                v[4 * k + 3] = (p1 >> 2) & kM3;
+            } else {
+                v[4 * k + 0] = (p0 >> 1) & kM1;
+                v[4 * k + 1] = (p1 >> 1) & kM1;
+                v[4 * k + 2] = (p0 >> 3) & kM1;
+                v[4 * k + 3] = (p1 >> 3) & kM1;
+            }
         } else {
-            const uint32_t hi = (MODE == 1) ? ~hs[uu] : hs[uu];
-            v[uu * 4 + 0] = ((hi << 1) & 0x22222222u) | (lo & 0x11111111u);
-            v[uu * 4 + 1] = (hi & 0x22222222u) | ((lo >> 1) & 0x11111111u);
-            v[uu * 4 + 2] = ((hi >> 1) & 0x22222222u) | ((lo >> 2) & 0x11111111u);
-            v[uu * 4 + 3] = ((hi >> 2) & 0x22222222u) | ((lo >> 3) & 0x11111111u);
+            const uint32_t c = (MODE == 5) ? ~w[k] : w[k];   // words 0..7 only
+            v[4 * k + 0] = c & kM1;
+            v[4 * k + 1] = (c >> 1) & kM1;
+            v[4 * k + 2] = (c >> 2) & kM1;
+            v[4 * k + 3] = (c >> 3) & kM1;
         }
     }
 }
 
-// One pass of one row: 4 x (8 hi + 8 lo words from the swizzled SMEM tiles ->
-// 32 A registers -> tcgen05.st of 32 TMEM columns).
+// One pass of one row.  Paired storage: the pass's 32 blocks are 64 words in
+// two 16 KiB stages (t0: blocks 0..15, t1: 16..31); canonical: 32 words in one
+// stage.  All of the row's 16-byte chunks are read from the swizzled tiles
+// first (128B swizzle: chunk c of row m at c ^ (m & 7)), the stages go back to
+// the TMA producer, then A is built and stored to TMEM (4 x 32 columns).
 template <int MODE>
-__device__ __forceinline__ void convert_pass(uint32_t thi, uint32_t tlo, uint32_t swz, uint32_t dst, int dbg) {
-#pragma unroll 1
+__device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, int dbg,
+                                             uint64_t* rel0, uint64_t* rel1, int lane) {
+    constexpr bool kPair = MODE <= 3;
+    uint4 q[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t off = (((uint32_t)c) ^ swz) << 4;
+        q[c] = lds128(t0 + off);
+        if (kPair) q[8 + c] = lds128(t1 + off);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        mbar_arrive(rel0);
+        if (kPair) mbar_arrive(rel1);
+    }
+#pragma unroll
     for (int b4 = 0; b4 < 4; ++b4) {
-        // 128B swizzle: 16-byte chunk c of row m lives at chunk c ^ (m & 7)
-        const uint32_t c0 = (((uint32_t)(2 * b4)) ^ swz) << 4;
-        const uint32_t c1 = (((uint32_t)(2 * b4 + 1)) ^ swz) << 4;
-        const uint4 l0 = lds128(tlo + c0), l1 = lds128(tlo + c1);
-        uint4 h0 = l0, h1 = l1;
-        if (MODE <= 1) {
-            h0 = lds128(thi + c0);
-            h1 = lds128(thi + c1);
-        }
         uint32_t v[32];
-        build_a<MODE>(h0, h1, l0, l1, v);
+        if (kPair) {
+            const uint4 qq[4] = {q[4 * b4], q[4 * b4 + 1], q[4 * b4 + 2], q[4 * b4 + 3]};
+            build_a<MODE>(qq, v);
+        } else {
+            const uint4 qq[4] = {q[2 * b4], q[2 * b4 + 1], q[2 * b4], q[2 * b4 + 1]};
+            build_a<MODE>(qq, v);
+        }
         if (dbg != 1 && dbg != 3)
             st_tmem_x32(dst + (uint32_t)(32 * b4), v);
         else if (v[0] == 0x12345 && v[3] == 0x777)
@@ -201,9 +261,9 @@ __device__ __forceinline__ void convert_pass(uint32_t thi, uint32_t tlo, uint32_
 #define TWAIT(bar, ph, slotid)                                   \
     do {                                                         \
         if (p.prof) {                                            \
-            const long long _t0 = clock64();                     \
+            const long long _t0 = gtimer();                      \
             mbar_wait(bar, ph);                                  \
-            prof[slotid] += clock64() - _t0;                     \
+            prof[slotid] += gtimer() - _t0;                      \
         } else {                                                 \
             mbar_wait(bar, ph);                                  \
         }                                                        \
@@ -218,6 +278,7 @@ struct TcPlan {
     int chunks;       // 32-word K-chunks per tile
     long long units;  // tiles * chunks
     int slots, sf_col, d_col;
+    int wstages;      // weight tile ring depth
     int passes;       // ceil(k_used / 2): layer pairs (0,1), (2,3), ...
     int Gp;           // passes per accumulator group (<= G/2 layers pairs, K * 2^G <= 2^24)
     int regions;      // ceil(passes / Gp)
@@ -262,19 +323,168 @@ __device__ __forceinline__ Seg segment(const TcPlan& p, long long u, long long u
     return s;
 }
 
+// Fused steps a1-a2 (same arithmetic as pb_act.cu) run by
+// the 256 converter threads before the MMAs: every CTA takes max|x[b,:]| itself
+// (an L2-resident re-read of B*K floats), casts and bit-transposes 1/G of the
+// (b, word) items into the B operand tiles in the workspace, and a grid barrier
+// publishes them; meanwhile warp 0 already streams weight tiles.
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+template <int NPAD>
+__device__ __forceinline__ void fused_act_prologue(const GemmArgs& g, const TcPlan& p, Bars& bars, int pt,
+                                                   uint8_t* bstage0, int kc0) {
+    const int cw = pt >> 5, lane = pt & 31;
+    long long tpw = 0, tmax = 0, ttr = 0, tgb = 0;
+    pdl_wait();                                   // x may be the previous kernel's output
+    if (g.tl) tpw = gtimer();
+    const int B = (int)g.B;
+    // this CTA's (b, word) items: words up to the last chunk's end (zero B for the K
+    // tail, where the complemented sign layer is 1); warp cw takes items i0 + cw + 8k
+    const int64_t Wt = (int64_t)p.chunks * kChunkWords, N = (int64_t)B * Wt;
+    const int64_t G = gridDim.x;
+    const int64_t i0 = N * blockIdx.x / G, i1 = N * (blockIdx.x + 1) / G;
+    auto item_x = [&](int64_t it) -> float {
+        const int b = (int)(it / Wt);
+        const int64_t c = 32 * (it - (int64_t)b * Wt) + lane;
+        return c < g.K ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
+    };
+    // the first two slice items' and four first-chunk items' values are loaded with
+    // the max wave (one L2 round trip); the grid-barrier generation is read now too
+    const float xv0 = (i0 + cw < i1) ? item_x(i0 + cw) : 0.f;
+    const float xv1 = (i0 + cw + 8 < i1) ? item_x(i0 + cw + 8) : 0.f;
+    auto chunk_x = [&](int64_t it) -> float {   // first-chunk item it = b * 32 + local word
+        const int b = (int)(it / kChunkWords);
+        const int64_t c = 32 * ((int64_t)kc0 * kChunkWords + (it - (int64_t)b * kChunkWords)) + lane;
+        return (b < B && c < g.K) ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
+    };
+    float cx[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) cx[k] = chunk_x(cw + 8 * k);
+    if (pt == 0) bars.gen = ld_acquire_gpu(g.gbar + 1);
+    // ---- a1 (part 1): max|x[b,:]|
+    const bool vec = (g.K & 3) == 0 && (reinterpret_cast<uintptr_t>(g.x) & 15) == 0;
+    for (int b = 0; b < B; ++b) {
+        const float* xb = g.x + (int64_t)b * g.K;
+        float m = 0.f;
+        if (vec) {
+            const float4* x4 = reinterpret_cast<const float4*>(xb);
+            const int64_t n4 = g.K / 4;
+            for (int64_t c0 = pt; c0 < n4; c0 += 16 * 256) {    // 16 loads in flight per thread
+                float4 v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int64_t c = c0 + (int64_t)u * 256;
+                    v[u] = c < n4 ? __ldg(x4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+            }
+        } else {
+            for (int64_t c = pt; c < g.K; c += 256) m = fmaxf(m, fabsf(__ldg(xb + c)));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) bars.red[cw * kTcMaxN + b] = m;
+    }
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    if (g.tl) tmax = gtimer();
+    if (pt < B) {
+        float m = bars.red[pt];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) m = fmaxf(m, bars.red[w * kTcMaxN + pt]);
+        bars.f[pt] = (g.act_frac == kActAutoFrac) ? act_frac_of(m, g.a) : g.act_frac;
+        bars.xs[pt] = 0;
+    }
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    // ---- a1 (part 2) + a2: cast, ballot-transpose, B operand tiles
+    int k = 0;
+    for (int64_t it = i0 + cw; it < i1; it += 8, ++k) {
+        const int b = (int)(it / Wt);
+        const int64_t w = it - (int64_t)b * Wt;
+        const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
+        const long long q = act_cast(v, bars.f[b], g.a);
+        uint32_t mine = 0;
+        for (int j = 0; j < g.a; ++j) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (unsigned)((q >> (g.a - 1 - j)) & 1));
+            if (lane == j) mine = word;
+        }
+        if (lane < g.a) put_b_operand(g.bexp, NPAD, w, b * g.a + lane, mine);
+        if (b == B - 1 && B * g.a + lane < NPAD) put_b_operand(g.bexp, NPAD, w, B * g.a + lane, 0u);
+        long long xs = q;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        if (lane == 0) atomicAdd(&bars.xs[b], (unsigned long long)xs);
+    }
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    if (pt < B) {
+        g.xsum[(int64_t)pt * kXsumStride + blockIdx.x] = (long long)bars.xs[pt];
+        if (blockIdx.x == 0) g.f[pt] = bars.f[pt];
+    }
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    if (g.tl) ttr = gtimer();
+    // ---- grid barrier, arrive side (generation-based; the arrival count is left
+    // zero).  The CTA's writes are ordered before thread 0's release by bar.sync and
+    // a cumulative fence; warp 2 waits for the generation change before copying
+    // other CTAs' tiles, so the converters go straight on.
+    if (pt == 0) {
+        __threadfence();
+        const int old = atomicAdd(g.gbar, 1);
+        if (old == (int)G - 1) {
+            __threadfence();
+            atomicAdd(g.gbar + 1, 1);             // release the waiters first ...
+            atomicExch(g.gbar, 0);                // ... then clear the count for the next call
+        }
+    }
+    asm volatile("bar.arrive 3, 288;" ::: "memory");
+    // ---- the CTA's first chunk, built straight into B stage 0 (same tile layout)
+    auto chunk_item = [&](int64_t it, float v) {
+        const int b = (int)(it / kChunkWords);
+        const int wl = (int)(it - (int64_t)b * kChunkWords);
+        const long long q = act_cast(v, bars.f[b], g.a);
+        uint32_t mine = 0;
+        for (int j = 0; j < g.a; ++j) {
+            const uint32_t word = __ballot_sync(0xffffffffu, (unsigned)((q >> (g.a - 1 - j)) & 1));
+            if (lane == j) mine = word;
+        }
+        if (lane < g.a) put_b_operand(bstage0, NPAD, wl, b * g.a + lane, mine);
+        if (b == B - 1 && B * g.a + lane < NPAD) put_b_operand(bstage0, NPAD, wl, B * g.a + lane, 0u);
+    };
+    const int64_t nci = (int64_t)B * kChunkWords;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (cw + 8 * k < nci) chunk_item(cw + 8 * k, cx[k]);
+    for (int64_t it = cw + 32; it < nci; it += 8) chunk_item(it, chunk_x(it));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA operand reads
+    asm volatile("bar.sync 2, 256;" ::: "memory");
+    if (pt == 0) mbar_arrive(&bars.b_full[0]);
+    if (g.tl && pt == 0) {
+        tgb = gtimer();
+        long long* r = tl_record(g.tl);
+        if (r) {
+            const long long rec[10] = {2, blockIdx.x, 0, 0, tpw, tmax, ttr, tgb, 0, 0};
+            for (int q = 0; q < 10; ++q) r[q] = rec[q];
+        }
+    }
+}
+
 template <int NPAD>
 __global__ void __launch_bounds__(kThreads, 1)
-bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUtensorMap wmap)
+bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUtensorMap pmap,
+                  const __grid_constant__ CUtensorMap smap)
 {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzled TMA tiles
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars& bars = *reinterpret_cast<Bars*>(smem);
-    uint8_t* wtile0 = smem + 1024;
-    uint8_t* btile0 = wtile0 + kWStages * kWTileBytes;
-    unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(btile0 + 2 * kBStageMax);  // [b][128]
+    uint8_t* wtile0 = smem + kHdrBytes;
     constexpr uint32_t kBTile = NPAD * 32;                    // one MMA's B (64 columns)
     constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;  // one K-chunk (16 MMAs)
+    uint8_t* btile0 = wtile0 + p.wstages * kWTileBytes;
+    unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(btile0 + 2 * kBStage);  // [b][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long G = gridDim.x;
@@ -289,7 +499,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             mbar_init(&bars.a_full[s], 4);               // the 4 converter warps of one h-set
             mbar_init(&bars.a_empty[s], 1);
         }
-        for (int s = 0; s < kWStages; ++s) {
+        for (int s = 0; s < p.wstages; ++s) {
             mbar_init(&bars.w_full[s], 1);
             mbar_init(&bars.w_empty[s], 4);              // the h-set that converts the tile
         }
@@ -299,8 +509,10 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         }
         mbar_init(&bars.d_full, 1);
         mbar_init(&bars.d_empty, 4);
+        mbar_init(&bars.x_ready, 1);
         fence_mbar_init();
-        asm volatile("prefetch.tensormap [%0];" ::"l"(&wmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&pmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&smap) : "memory");
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -343,25 +555,59 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         for (long long u = u0; u < u1;) {
             const Seg sg = segment(p, u, u1);
             for (int kc = sg.kcA; kc < sg.kcB; ++kc)
-                for (int i = 0; i < g.k_used; ++i, ++tc) {
-                    const int st = tc % kWStages;
-                    TWAIT(&bars.w_empty[st], (uint32_t)(((tc / kWStages) & 1) ^ 1), 0);
-                    if (elect_one()) {
-                        mbar_arrive_expect_tx(&bars.w_full[st], kWTileBytes);
-                        tma_load_3d(wtile0 + st * kWTileBytes, &wmap, kc * kChunkWords, sg.rt * kTcRows, i,
-                                    &bars.w_full[st]);
+                for (int ps = 0; ps < p.passes; ++ps) {
+                    // a stored pair: two 32-word boxes of the pair row; else the canonical last layer
+                    const bool stored_pair = 2 * ps + 1 < g.L;
+                    for (int t = 0; t < (stored_pair ? 2 : 1); ++t, ++tc) {
+                        const int st = tc % p.wstages;
+                        TWAIT(&bars.w_empty[st], (uint32_t)(((tc / p.wstages) & 1) ^ 1), 0);
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(&bars.w_full[st], kWTileBytes);
+                            if (stored_pair)
+                                tma_load_3d(wtile0 + st * kWTileBytes, &pmap, kc * 2 * kChunkWords + t * kChunkWords,
+                                            sg.rt * kTcRows, ps, &bars.w_full[st]);
+                            else
+                                tma_load_3d(wtile0 + st * kWTileBytes, &smap, kc * kChunkWords, sg.rt * kTcRows, 0,
+                                            &bars.w_full[st]);
+                        }
+                        __syncwarp();
                     }
-                    __syncwarp();
                 }
             u = sg.next;
         }
     } else if (warp == 2) {
         // ------------------------------------------------ B (plane tile) producer
-        pdl_wait();
+        // Fused path: the converters build the CTA's first chunk in stage 0 themselves
+        // (no copy); later chunks are copied once the grid barrier has published them.
+        if (!g.x) pdl_wait();
+        bool published = false;
+        auto wait_published = [&]() {
+            if (g.x && !published) {
+                asm volatile("bar.sync 3, 288;" ::: "memory");         // this CTA has arrived
+                while (ld_acquire_gpu(g.gbar + 1) == bars.gen) __nanosleep(64);   // ... and every other
+                asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> bulk-copy reads
+                if (g.tl && lane == 0) bars.t_b = gtimer();
+                // sum_c x_q[b, c] from every CTA's partial, for the epilogue
+                for (int b = 0; b < (int)g.B; ++b) {
+                    unsigned long long t = 0;
+                    for (int c = lane; c < (int)G; c += 32)
+                        t += (unsigned long long)__ldcg(g.xsum + (int64_t)b * kXsumStride + c);
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                    if (lane == 0) bars.xsum[b] = t;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars.x_ready);
+                published = true;
+            }
+        };
+        if (!g.x && g.tl && lane == 0) bars.t_b = gtimer();
         int cc = 0;
         for (long long u = u0; u < u1;) {
             const Seg sg = segment(p, u, u1);
             for (int kc = sg.kcA; kc < sg.kcB; ++kc, ++cc) {
+                if (g.x && cc == 0) continue;                 // built in place by the converters
+                wait_published();
                 const int st = cc & 1;
                 mbar_wait(&bars.b_empty[st], (uint32_t)(((cc >> 1) & 1) ^ 1));
                 if (elect_one()) {
@@ -372,6 +618,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             }
             u = sg.next;
         }
+        wait_published();                                     // (a one-chunk CTA still joins bar 3)
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer: the whole warp walks the
         // schedule (warp-uniform values stay in uniform registers), one elected lane issues.
@@ -379,6 +626,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(NPAD >> 3) << 17) | (1u << 23) |
                                ((uint32_t)(kTcRows >> 4) << 24);
         const uint32_t sfa = tmem + p.sf_col;
+        long long t_mma0 = 0;
         uint32_t slot = 0, phase = 0;
         int cc = 0, seg = 0;
         for (long long u = u0; u < u1; ++seg) {
@@ -399,6 +647,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     const bool open = first && kc == sg.kcA;
                     TWAIT(&bars.a_full[slot], phase, 2);
                     tc_fence_after();
+                    if (g.tl && t_mma0 == 0) t_mma0 = gtimer();
                     if (p.dbg == 2 || p.dbg == 3) {
                         if (elect_one()) tc_commit(&bars.a_empty[slot]);
                     } else if (elect_one()) {
@@ -423,6 +672,10 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             __syncwarp();
             u = sg.next;
         }
+        if (g.tl && lane == 0) {
+            bars.t_mma0 = t_mma0;
+            bars.t_mend = gtimer();
+        }
     } else {
         // ------------------------------------------------ converters (+ epilogue)
         const int cw = warp - kConv0;
@@ -432,15 +685,24 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const uint32_t wtile_s = smem_u32(wtile0) + (uint32_t)m * 128;
         const uint32_t swz = (uint32_t)(m & 7);
+        if (g.x) fused_act_prologue<NPAD>(g, p, bars, threadIdx.x - kConv0 * 32, btile0, (int)(u0 % p.chunks));
         int tc = 0, pc = 0, seg = 0;
         // passes (kc, ps) in issue order; h-set h converts passes pc = h, h + 2, ...; pass pc
         // uses A slot pc % slots; its tiles are tc (hi, if paired) and tc + 1 (or tc alone)
         int slot = h % p.slots, sphase = (h / p.slots) & 1;
         // software pipeline: the TMEM stores of one pass drain while the next is awaited
         int pend_slot = -1;
+        long long tf[4] = {0, 0, 0, 0};   // timeline: first pass w_full, a_empty, converted, published
         auto publish = [&]() {
             if (pend_slot >= 0) {
-                tmem_st_wait();
+                if (g.tl && tf[3] == 0 && tf[2] != 0) tf[3] = gtimer();
+                if (p.prof) {
+                    const long long t0 = gtimer();
+                    tmem_st_wait();
+                    prof[1] += gtimer() - t0;         // converters: TMEM store drain (ns)
+                } else {
+                    tmem_st_wait();
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.a_full[pend_slot]);
@@ -453,34 +715,41 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             const bool row_ok = row < g.R;
             for (int kc = sg.kcA; kc < sg.kcB; ++kc) {
                 for (int ps = 0; ps < p.passes; ++ps, ++pc) {
-                    const bool paired = 2 * ps + 1 < g.k_used;
-                    const int ntile = paired ? 2 : 1;
+                    const bool stored_pair = 2 * ps + 1 < g.L;
+                    const bool use_lo = 2 * ps + 1 < g.k_used;
+                    const int ntile = stored_pair ? 2 : 1;
                     if ((pc & 1) != h) {
                         tc += ntile;
                         continue;
                     }
-                    const int st_hi = tc % kWStages, st_lo = (tc + ntile - 1) % kWStages;
-                    TWAIT(&bars.w_full[st_hi], (uint32_t)((tc / kWStages) & 1), 3);
-                    if (paired)
-                        TWAIT(&bars.w_full[st_lo], (uint32_t)(((tc + 1) / kWStages) & 1), 3);
+                    if (PB_PUBLISH_EARLY) publish();    // previous pass's A is in TMEM: tell the MMA
+                    const int st_hi = tc % p.wstages, st_lo = (tc + ntile - 1) % p.wstages;
+                    TWAIT(&bars.w_full[st_hi], (uint32_t)((tc / p.wstages) & 1), 3);
+                    if (stored_pair)
+                        TWAIT(&bars.w_full[st_lo], (uint32_t)(((tc + 1) / p.wstages) & 1), 3);
+                    if (g.tl && tf[0] == 0) tf[0] = gtimer();
                     const uint32_t thi = wtile_s + (uint32_t)st_hi * kWTileBytes;
                     const uint32_t tlo = wtile_s + (uint32_t)st_lo * kWTileBytes;
-                    publish();                          // previous pass's A is in TMEM: tell the MMA
+                    if (!PB_PUBLISH_EARLY) publish();
                     TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
+                    if (g.tl && tf[1] == 0) tf[1] = gtimer();
                     tc_fence_after();
-                    const int mode = paired ? (ps == 0 ? 1 : 0) : (ps == 0 ? 3 : 2);
+                    const int mode = stored_pair ? (use_lo ? 0 : 2) + (ps == 0 ? 1 : 0) : (ps == 0 ? 5 : 4);
                     const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
+                    uint64_t* rhi = &bars.w_empty[st_hi];
+                    uint64_t* rlo = &bars.w_empty[st_lo];
+                    const long long tcv = p.prof ? gtimer() : 0;
                     switch (mode) {
-                        case 0: convert_pass<0>(thi, tlo, swz, dst, p.dbg); break;
-                        case 1: convert_pass<1>(thi, tlo, swz, dst, p.dbg); break;
-                        case 2: convert_pass<2>(thi, tlo, swz, dst, p.dbg); break;
-                        default: convert_pass<3>(thi, tlo, swz, dst, p.dbg); break;
+                        case 0: convert_pass<0>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
+                        case 1: convert_pass<1>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
+                        case 2: convert_pass<2>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
+                        case 3: convert_pass<3>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
+                        case 4: convert_pass<4>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
+                        default: convert_pass<5>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
                     }
-                    __syncwarp();                       // this warp's words are in TMEM-bound registers
-                    if (lane == 0) {
-                        mbar_arrive(&bars.w_empty[st_hi]);
-                        if (paired) mbar_arrive(&bars.w_empty[st_lo]);
-                    }
+                    if (p.prof) prof[0] += gtimer() - tcv;   // converters: LDS + build + STTM issue (ns)
+                    if (g.tl && tf[2] == 0) tf[2] = gtimer();
+
                     tc += ntile;
                     pend_slot = slot;
                     slot += 2;
@@ -496,32 +765,39 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 // ---------------- epilogue: fold the accumulators into exact int64
                 mbar_wait(&bars.d_full, (uint32_t)(seg & 1));
                 tc_fence_after();
+                long long te[4] = {0, 0, 0, 0};
+                if (g.tl) te[0] = gtimer();
                 pdl_wait();
                 // tot_b = sum_j T_j sum_r |S_lo(r)| D_r[b*a + j] (+ the sign correction below);
                 // lo(r) = least significant layer of group r
-                for (int b = 0; b < g.B; ++b) s_tot[b * kTcRows + m] = 0;
                 for (int r = 0; r < p.regions; ++r) {
                     int last = (r + 1) * p.Gp - 1;
                     if (last > p.passes - 1) last = p.passes - 1;
                     const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
-#pragma unroll 1
-                    for (int c = 0; c < NPAD; c += 8) {
-                        uint32_t t8[8];
-                        ld_tmem_x8(tmem + lane_off + (uint32_t)(p.d_col + r * NPAD + c), t8);
-                        tmem_ld_wait();
+                    uint32_t dv[NPAD];
+                    ld_tmem_cols<NPAD>(tmem + lane_off + (uint32_t)(p.d_col + r * NPAD), dv);
+                    tmem_ld_wait();
+                    // columns n = b*a + j in order: one register sum per batch column
+                    unsigned long long acc = 0;
+                    int j = 0, bc = 0;
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const int n = c + e, b = n / g.a, j = n - b * g.a;
-                            if (b < g.B)
-                                s_tot[b * kTcRows + m] +=
-                                    plane_scale(g.a, j) *
-                                    (wr * (unsigned long long)__float2uint_rn(__uint_as_float(t8[e])));
+                    for (int n = 0; n < NPAD; ++n) {
+                        if (bc < g.B) {
+                            acc += plane_scale(g.a, j) * (wr * (unsigned long long)__float2uint_rn(__uint_as_float(dv[n])));
+                            if (++j == g.a) {
+                                if (r == 0) s_tot[bc * kTcRows + m] = acc;
+                                else s_tot[bc * kTcRows + m] += acc;
+                                acc = 0;
+                                j = 0;
+                                ++bc;
+                            }
                         }
                     }
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.d_empty);
+                if (g.tl) te[1] = gtimer();
                 auto tot_of = [&](int b) -> unsigned long long { return s_tot[b * kTcRows + m]; };
                 const bool whole = (sg.kcA == 0 && sg.kcB == p.chunks);
                 bool finalize = whole;
@@ -531,19 +807,22 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     const int myslot = (u == u0) ? 0 : 1;
                     unsigned long long* sl = g.slots + (((int64_t)blockIdx.x * 2 + myslot) * g.B) * kTcRows;
                     for (int b = 0; b < g.B; ++b) sl[b * kTcRows + m] = tot_of(b);
-                    __threadfence();
+                    // the 128 threads' slot stores are ordered before the counter update by
+                    // bar.sync + thread 0's cumulative fence; symmetrically on the acquire side
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (cw == 0 && lane == 0) {
+                        __threadfence();
                         const int add = sg.kcB - sg.kcA;
                         const int old = atomicAdd(&g.counters[sg.rt], add);
                         const int last = (old + add == p.chunks);
                         if (last) g.counters[sg.rt] = 0;      // every call leaves the counters zero
                         bars.last_flag = last;
+                        __threadfence();
                     }
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     finalize = bars.last_flag != 0;
-                    if (finalize) __threadfence();
                 }
+                if (g.tl) te[2] = gtimer();
                 if (finalize && row_ok) {
                     for (int b = 0; b < g.B; ++b) {
                         unsigned long long t;
@@ -567,34 +846,66 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                             // (o - |S_0|) * sum_c x_q: the binary offset (o = 1) and the
                             // complemented sign layer (file header)
                             unsigned long long sx = 0;
-                            for (int pp = 0; pp < g.nsplit; ++pp)
-                                sx += (unsigned long long)g.xsum[(int64_t)b * kMaxSplit + pp];
+                            if (g.x) {
+                                mbar_wait(&bars.x_ready, 0);
+                                sx = bars.xsum[b];
+                            }
+                            else
+                                for (int pp = 0; pp < g.nsplit; ++pp)
+                                    sx += (unsigned long long)g.xsum[(int64_t)b * kXsumStride + pp];
                             t += ((unsigned long long)g.offset - layer_mag(g.L, g.offset, 0)) * sx;
                         }
                         const long long accv = (long long)t;
                         const int64_t o = (int64_t)b * g.R + row;
                         if (g.acc) g.acc[o] = accv;
-                        float yv = dequant(accv, g.scale, g.f[b]);
+                        float yv = dequant(accv, g.scale, g.x ? bars.f[b] : g.f[b]);
                         if (g.bias) yv += g.bias[row];
                         if (g.accumulate) yv += g.y[o];
                         g.y[o] = apply_fn(yv, g.fn);
                     }
                 }
+                if (g.tl && cw == 0 && lane == 0) {
+                    te[3] = gtimer();
+                    long long* r = tl_record(g.tl);
+                    if (r) {
+                        const long long rec[10] = {3, blockIdx.x, seg, (whole ? 1 : 0) + (finalize ? 2 : 0),
+                                                   te[0], te[1], te[2], te[3], 0, 0};
+                        for (int q = 0; q < 10; ++q) r[q] = rec[q];
+                    }
+                }
             }
             u = sg.next;
         }
+        if (g.tl && warp == kConv0 && lane == 0) {
+            bars.t_cend = gtimer();
+            long long* r = tl_record(g.tl);
+            if (r) {
+                const long long rec[10] = {5, blockIdx.x, 0, 0, tf[0], tf[1], tf[2], tf[3], 0, 0};
+                for (int q = 0; q < 10; ++q) r[q] = rec[q];
+            }
+        }
     }
 
-    if (p.prof && blockIdx.x == 0 && lane == 0)
-        printf("warp %d total %lld  w_empty %lld b_full %lld a_full %lld w_full %lld a_empty %lld\n", warp,
-               clock64() - t_start, prof[0], prof[1], prof[2], prof[3], prof[4]);
-    if (p.dbg == 6 && warp == 1 && lane == 0) {
-        unsigned smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        long long gt;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-        printf("cta %d sm %u units %lld cycles %lld end_ns %lld start_ns %lld\n", blockIdx.x, smid, u1 - u0,
-               clock64() - t_start, gt, g_start);
+    if (p.prof && g.tl && lane == 0) {
+        // wait totals (ns): w_empty, b_full, a_full, w_full, a_empty
+        long long* r = tl_record(g.tl);
+        if (r) {
+            const long long rec[10] = {4, blockIdx.x, warp, gtimer() - g_start, prof[0], prof[1], prof[2], prof[3],
+                                       prof[4], 0};
+            for (int q = 0; q < 10; ++q) r[q] = rec[q];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (g.tl && warp == 1 && lane == 0) {
+        long long* r = tl_record(g.tl);
+        if (r) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            const long long rec[10] = {1, blockIdx.x, smid, u1 - u0, g_start, bars.t_b, bars.t_mma0, bars.t_mend,
+                                       bars.t_cend, gtimer()};
+            for (int k = 0; k < 10; ++k) r[k] = rec[k];
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -606,7 +917,12 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-cudaError_t make_weight_map(const GemmArgs& g, CUtensorMap* map)
+// Tensor maps of the stored weights (pb.h), box {32 words, 128 rows, 1}, 128B
+// swizzle; out-of-range rows / words (tile tails) are filled with zeros:
+//   pmap: the L/2 layer pairs as {2*kwords, R, L/2} (pair rows of 2*kwords words);
+//   smap: the canonical last layer of an odd L as {kwords, R, 1}.
+// A map the shape does not have is a copy of the other (never read).
+cudaError_t make_weight_maps(const GemmArgs& g, CUtensorMap* pmap, CUtensorMap* smap)
 {
     static EncodeTiledFn encode = nullptr;
     if (!encode) {
@@ -616,15 +932,21 @@ cudaError_t make_weight_map(const GemmArgs& g, CUtensorMap* map)
         if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
         encode = reinterpret_cast<EncodeTiledFn>(fn);
     }
-    // bits[L][R][kwords] uint32 as a 3-D tensor {kwords, R, L}; box {32 words, 128 rows, 1}.
-    // Out-of-range rows / words (tile tails) are filled with zeros by the TMA unit.
-    const cuuint64_t dims[3] = {(cuuint64_t)g.kwords, (cuuint64_t)g.R, (cuuint64_t)g.L};
-    const cuuint64_t strides[2] = {(cuuint64_t)g.kwords * 4, (cuuint64_t)g.kwords * 4 * (cuuint64_t)g.R};
     const cuuint32_t box[3] = {kChunkWords, kTcRows, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(g.bits), dims, strides, box,
-                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    auto enc = [&](CUtensorMap* m, const uint32_t* base, cuuint64_t w, cuuint64_t depth) {
+        const cuuint64_t dims[3] = {w, (cuuint64_t)g.R, depth};
+        const cuuint64_t strides[2] = {w * 4, w * 4 * (cuuint64_t)g.R};
+        return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<uint32_t*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    };
+    CUresult r = CUDA_SUCCESS;
+    if (g.L >= 2) r = enc(pmap, g.bits, 2 * (cuuint64_t)g.kwords, (cuuint64_t)(g.L / 2));
+    if (r == CUDA_SUCCESS && (g.L & 1))
+        r = enc(smap, g.bits + (int64_t)(g.L - 1) * g.R * g.kwords, (cuuint64_t)g.kwords, 1);
+    if (g.L < 2) *pmap = *smap;
+    if (!(g.L & 1)) *smap = *pmap;
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
@@ -675,7 +997,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     }
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kSmemBytes);
+                                             (int)kSmemMax);
         if (e != cudaSuccess) return e;
         cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              (int)cudaSharedmemCarveoutMaxShared);
@@ -683,25 +1005,31 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     }
     TcPlan p;
     if (!make_plan(g, NPAD, p)) return cudaErrorNotSupported;
-    CUtensorMap map;
-    cudaError_t e = make_weight_map(g, &map);
+    CUtensorMap pmap, smap;
+    cudaError_t e = make_weight_maps(g, &pmap, &smap);
     if (e != cudaSuccess) return e;
     p.dbg = dbg;
     p.prof = prof;
+    // weight ring: every 16 KiB stage the B stages and epilogue sums leave free
+    const uint32_t fixed = 1024 + kHdrBytes + 2 * (kChunkWords / 2) * NPAD * 32 + (uint32_t)g.B * kTcRows * 8;
+    p.wstages = (int)((kSmemMax - fixed) / kWTileBytes);
+    if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
+    if (p.wstages < 4) return cudaErrorNotSupported;
+    const uint32_t smem = fixed + (uint32_t)p.wstages * kWTileBytes;
     long long grid = p.units < sms ? p.units : sms;
     if (grid > kMaxCtas) grid = kMaxCtas;
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = kSmemBytes;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute la[1];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = la;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, bitgemm_tc_kernel<NPAD>, g, p, map);
+    return cudaLaunchKernelEx(&cfg, bitgemm_tc_kernel<NPAD>, g, p, pmap, smap);
 }
 
 }  // namespace

@@ -6,8 +6,9 @@
 //   a5  y   = (float) ldexp((double)acc * s_w, -f_b)             (G13)
 //
 // One warp per output row (grid-stride).  Lanes stream the row's packed
-// weight words with coalesced 128-bit non-allocating loads (4 words = 128
-// columns per lane per load) and AND/POPC them against the activation planes,
+// weight words with coalesced 128-bit non-allocating loads (a stored layer
+// pair: 64 columns of both layers per load, de-interleaved into the two layer
+// words with 4 logic ops, pb.h) and AND/POPC them against the activation planes,
 // which one thread stages into shared memory per CTA with a 1-D TMA bulk
 // copy (cp.async.bulk -> UBLKCP) completing on an mbarrier.  Planes are laid
 // out [a][kwords] so a lane's LDS.128 hits 4 consecutive banks: conflict-free.
@@ -78,31 +79,70 @@ bitgemv_popc_kernel(const GemmArgs g)
 
     for (int64_t r = (int64_t)blockIdx.x * kWarps + warp; r < g.R; r += (int64_t)gridDim.x * kWarps) {
         unsigned long long tot = 0;
-        for (int i = 0; i < g.k_used; ++i) {
-            const uint4* wrow = reinterpret_cast<const uint4*>(g.bits + ((int64_t)i * g.R + r) * g.kwords);
-            uint32_t cnt[APAD];
+        for (int i = 0; i < g.k_used;) {
+            if (i + 1 < g.L) {
+                // stored pair (i, i+1) (pb.h): one 128-bit load = blocks 2v, 2v+1 of both
+                // layers; de-interleave the (lower, upper) bit pairs back into layer words
+                const bool use_lo = i + 1 < g.k_used;
+                const uint4* prow = reinterpret_cast<const uint4*>(g.bits + ((int64_t)i * g.R + 2 * r) * g.kwords);
+                const uint2* P2 = reinterpret_cast<const uint2*>(P);
+                const int64_t kw2 = g.kwords / 2;
+                uint32_t ch[APAD], cl[APAD];
 #pragma unroll
-            for (int j = 0; j < APAD; ++j) cnt[j] = 0;
-            int64_t v = lane;
-            for (; v + 32 < kw4; v += 64) {
-                const uint4 w0 = ld_stream_u4(wrow + v);
-                const uint4 w1 = ld_stream_u4(wrow + v + 32);
-                and_popc<APAD>(w0, P, kw4, v, a, cnt);
-                and_popc<APAD>(w1, P, kw4, v + 32, a, cnt);
+                for (int j = 0; j < APAD; ++j) ch[j] = cl[j] = 0;
+                for (int64_t v = lane; v < kw2; v += 32) {
+                    const uint4 q = ld_stream_u4(prow + v);
+                    const uint32_t lo0 = (q.x & 0x55555555u) | ((q.y << 1) & 0xAAAAAAAAu);
+                    const uint32_t hi0 = ((q.x >> 1) & 0x55555555u) | (q.y & 0xAAAAAAAAu);
+                    const uint32_t lo1 = (q.z & 0x55555555u) | ((q.w << 1) & 0xAAAAAAAAu);
+                    const uint32_t hi1 = ((q.z >> 1) & 0x55555555u) | (q.w & 0xAAAAAAAAu);
+#pragma unroll
+                    for (int j = 0; j < APAD; ++j) {
+                        if (j < a) {
+                            const uint2 x = P2[j * kw2 + v];
+                            ch[j] += __popc(hi0 & x.x) + __popc(hi1 & x.y);
+                            if (use_lo) cl[j] += __popc(lo0 & x.x) + __popc(lo1 & x.y);
+                        }
+                    }
+                }
+                unsigned long long sh = 0, sl = 0;
+#pragma unroll
+                for (int j = 0; j < APAD; ++j)
+                    if (j < a) {
+                        sh += plane_scale(a, j) * (unsigned long long)ch[j];
+                        sl += plane_scale(a, j) * (unsigned long long)cl[j];
+                    }
+                tot += layer_scale(g.L, g.offset, i) * sh;
+                if (use_lo) tot += layer_scale(g.L, g.offset, i + 1) * sl;
+                i += 2;
+            } else {
+                // the canonical last layer of an odd L
+                const uint4* wrow = reinterpret_cast<const uint4*>(g.bits + ((int64_t)i * g.R + r) * g.kwords);
+                uint32_t cnt[APAD];
+#pragma unroll
+                for (int j = 0; j < APAD; ++j) cnt[j] = 0;
+                int64_t v = lane;
+                for (; v + 32 < kw4; v += 64) {
+                    const uint4 w0 = ld_stream_u4(wrow + v);
+                    const uint4 w1 = ld_stream_u4(wrow + v + 32);
+                    and_popc<APAD>(w0, P, kw4, v, a, cnt);
+                    and_popc<APAD>(w1, P, kw4, v + 32, a, cnt);
+                }
+                for (; v < kw4; v += 32) and_popc<APAD>(ld_stream_u4(wrow + v), P, kw4, v, a, cnt);
+                unsigned long long s = 0;
+#pragma unroll
+                for (int j = 0; j < APAD; ++j)
+                    if (j < a) s += plane_scale(a, j) * (unsigned long long)cnt[j];
+                tot += layer_scale(g.L, g.offset, i) * s;
+                i += 1;
             }
-            for (; v < kw4; v += 32) and_popc<APAD>(ld_stream_u4(wrow + v), P, kw4, v, a, cnt);
-            unsigned long long s = 0;
-#pragma unroll
-            for (int j = 0; j < APAD; ++j)
-                if (j < a) s += plane_scale(a, j) * (unsigned long long)cnt[j];
-            tot += layer_scale(g.L, g.offset, i) * s;
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
         if (lane == 0) {
             if (g.offset) {
                 unsigned long long sx = 0;
-                for (int p = 0; p < g.nsplit; ++p) sx += (unsigned long long)g.xsum[(int64_t)b * kMaxSplit + p];
+                for (int p = 0; p < g.nsplit; ++p) sx += (unsigned long long)g.xsum[(int64_t)b * kXsumStride + p];
                 tot += (unsigned long long)g.offset * sx;
             }
             const long long accv = (long long)tot;

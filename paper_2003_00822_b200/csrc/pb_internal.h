@@ -26,14 +26,17 @@ inline int tc_npad(int64_t batch, int32_t a) {
 // Workspace carve-up (documented in pb.h, pb_workspace_bytes):
 //   [tile counters int32 x kMaxTiles]   stream-K arrival counters; zero on
 //                                       entry, every call leaves them zero
+//   [grid barrier int32 x 2]            fused tensor-engine path: arrival
+//                                       count (left zero) + generation
 //   [partial slots int64 x kMaxCtas x 2 x B x 128]   tensor engine only
-//   [f_b int32 x B][Σx_q partials int64 x B x 64][bit planes [B][a][kwords]]
+//   [f_b int32 x B][Σx_q partials int64 x B x kXsumStride][bit planes [B][a][kwords]]
 //   [tensor-engine B operand tiles: one N_pad x 32-byte e2m1 tile per 2 words
 //    (64 columns), kwords rounded up to 32 words]
 // Every region except the counters is fully rewritten by each call, so one
 // zero-filled workspace can serve calls of any shape (not concurrently).
 constexpr int kMaxTiles = 8192;      // tensor engine: rows <= 8192 * 128
 constexpr int kMaxCtas = 160;        // tensor engine grid cap (B200: 148 SMs)
+constexpr int kXsumStride = kMaxCtas;   // Σx_q partials per batch column (act CTAs or fused GEMM CTAs)
 struct WsLayout {
     size_t off_count, off_slots, off_f, off_xsum, off_planes, off_bexp, total;
     int npad;
@@ -42,11 +45,11 @@ inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     WsLayout l;
     l.npad = tc_npad(batch, act_bits);
     l.off_count = 0;
-    l.off_slots = align_up(sizeof(int32_t) * kMaxTiles);
+    l.off_slots = align_up(sizeof(int32_t) * (kMaxTiles + 2));
     const size_t slots = l.npad ? sizeof(long long) * kMaxCtas * 2 * (size_t)batch * kTcRows : 0;
     l.off_f = align_up(l.off_slots + slots);
     l.off_xsum = align_up(l.off_f + sizeof(int32_t) * (size_t)batch);
-    l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kMaxSplit);
+    l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kXsumStride);
     l.off_bexp = align_up(l.off_planes + sizeof(uint32_t) * (size_t)batch * act_bits * kwords);
     l.total = align_up(l.off_bexp + (size_t)((kwords + 31) / 32 * 32) * 16 * (size_t)l.npad);
     return l;
@@ -65,8 +68,8 @@ struct GemmArgs {
     int L, offset, k_used, a;
     double scale;
     const uint32_t* planes; // [B][a][kwords]
-    const int32_t* f;       // [B]
-    const long long* xsum;  // [B][nsplit]
+    int32_t* f;             // [B]
+    long long* xsum;        // [B][kXsumStride], nsplit used
     int nsplit;
     int64_t B;
     float* y;               // [B][R]
@@ -76,10 +79,23 @@ struct GemmArgs {
     int accumulate;
     // tensor engine operands (valid when npad > 0)
     int npad;
-    const uint8_t* bexp;          // [kwords][npad x 32 canonical tile]
+    uint8_t* bexp;                // [kwords][npad x 32 canonical tile]
     unsigned long long* slots;    // [kMaxCtas][2][B][128] partial tile sums
     int* counters;                // [kMaxTiles]
+    long long* tl;                // diagnostics timeline (pb_debug_timeline) or null
+    // fused activation path (tensor engine, pb_matmul / pb_linear): when x is set the
+    // GEMM kernel itself runs steps a1-a2 (writing f, xsum, bexp) before the MMAs
+    const float* x;               // [B][K] or null
+    int64_t K;
+    int act_frac;
+    int* gbar;                    // grid barrier {arrival count, generation}
 };
+
+// Diagnostics timeline (PB_TC_DEBUG=6): device log, [0] = record counter,
+// records of 10 int64 from index 10; null when off.
+constexpr long long kTlRecords = 1 << 16;
+long long* debug_tl();
+
 
 cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kwords, int a,
                              int act_frac, void* ws, const WsLayout& l, cudaStream_t s);

@@ -17,7 +17,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
                  : "memory");
 }
 
-template <int STAGES, int BOXW, int BOXR>
+// ORDER 0: tiles in memory order (k fastest, then rows, then layers);
+// ORDER 1: the GEMM's order -- per (row tile, k chunk) unit all L layers, units contiguous per CTA.
+template <int STAGES, int BOXW, int BOXR, int ORDER>
 __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensorMap map, int kwords, int R, int L,
                                                  int* out) {
     extern __shared__ __align__(1024) uint8_t smraw[];
@@ -41,8 +43,18 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensor
         for (long long t = t0; t < t1; ++t, ++n) {
             const int st = n % STAGES;
             mbar_wait(&empty[st], ((n / STAGES) & 1) ^ 1);
-            const long long l = t / (tiles_k * tiles_r), rem = t - l * tiles_k * tiles_r;
-            const long long rt = rem / tiles_k, kt = rem - rt * tiles_k;
+            long long l, rt, kt;
+            if (ORDER == 0) {
+                l = t / (tiles_k * tiles_r);
+                const long long rem = t - l * tiles_k * tiles_r;
+                rt = rem / tiles_k;
+                kt = rem - rt * tiles_k;
+            } else {
+                const long long unit = t / L;
+                l = t - unit * L;
+                rt = unit / tiles_k;
+                kt = unit - rt * tiles_k;
+            }
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[st])), "r"(kTile)
                          : "memory");
             asm volatile(
@@ -68,7 +80,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-template <int STAGES, int BOXW, int BOXR>
+template <int STAGES, int BOXW, int BOXR, int ORDER = 0>
 void run(void* buf, int kwords, int R, int L) {
     static EncodeTiledFn enc = nullptr;
     if (!enc) {
@@ -86,20 +98,20 @@ void run(void* buf, int kwords, int R, int L) {
     int* d;
     cudaMalloc(&d, 4);
     const size_t smem = STAGES * BOXW * BOXR * 4 + 1024;
-    cudaFuncSetAttribute(stream<STAGES, BOXW, BOXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int i = 0; i < 3; ++i) stream<STAGES, BOXW, BOXR><<<148, 64, smem>>>(map, kwords, R, L, d);
+    cudaFuncSetAttribute(stream<STAGES, BOXW, BOXR, ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int i = 0; i < 3; ++i) stream<STAGES, BOXW, BOXR, ORDER><<<148, 64, smem>>>(map, kwords, R, L, d);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
     const int it = 10;
-    for (int i = 0; i < it; ++i) stream<STAGES, BOXW, BOXR><<<148, 64, smem>>>(map, kwords, R, L, d);
+    for (int i = 0; i < it; ++i) stream<STAGES, BOXW, BOXR, ORDER><<<148, 64, smem>>>(map, kwords, R, L, d);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     const double bytes = (double)kwords * 4 * R * L;
-    printf("stages %2d box %3dx%3d (%5d B): %.1f us  %.0f GB/s  %s\n", STAGES, BOXW, BOXR, BOXW * BOXR * 4,
+    printf("order %d stages %2d box %3dx%3d (%5d B): %.1f us  %.0f GB/s  %s\n", ORDER, STAGES, BOXW, BOXR, BOXW * BOXR * 4,
            ms * 1e3 / it, bytes / (ms * 1e-3 / it) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -108,11 +120,10 @@ int main() {
     void* buf;
     cudaMalloc(&buf, (size_t)kwords * 4 * R * L);
     cudaMemset(buf, 1, (size_t)kwords * 4 * R * L);
-    run<4, 32, 128>(buf, kwords, R, L);
-    run<8, 32, 128>(buf, kwords, R, L);
-    run<12, 32, 128>(buf, kwords, R, L);
-    run<8, 32, 256>(buf, kwords, R, L);
-    run<8, 64, 128>(buf, kwords, R, L);
-    run<4, 128, 64>(buf, kwords, R, L);
+    run<8, 32, 128, 0>(buf, kwords, R, L);
+    run<8, 32, 128, 1>(buf, kwords, R, L);
+    run<12, 32, 128, 1>(buf, kwords, R, L);
+    run<8, 32, 128, 0>(buf, kwords, R, L);
+    run<8, 32, 128, 1>(buf, kwords, R, L);
     return 0;
 }

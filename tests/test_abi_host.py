@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import synth
+from packed_layout import unpack_layers, unpack_layers_full
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -54,10 +55,7 @@ def _host_pack(pb, W, L, mode, clip=0.0):
 
 
 def _unpack(buf, L, R, K):
-    kw = 4 * ((K + 127) // 128)
-    words = buf[:L * R * kw].reshape(L, R, kw)
-    bits = np.unpackbits(words.view(np.uint8).reshape(L, R, kw * 4), axis=-1, bitorder="little")
-    return bits[:, :, :K]
+    return unpack_layers(buf, L, R, K)
 
 
 @pytest.mark.parametrize("R,K,L,mode", [(5, 37, 4, "grid"), (3, 128, 2, "grid"), (7, 300, 8, "grid"),
@@ -78,9 +76,7 @@ def test_packer_matches_oracle_decomposition(pb, orc, R, K, L, mode):
     assert np.array_equal(bits, ref)
     # padding columns are zero (AND-neutral)
     kw = 4 * ((K + 127) // 128)
-    full = np.unpackbits(buf[:L * R * kw].reshape(L, R, kw).view(np.uint8).reshape(L, R, kw * 4),
-                         axis=-1, bitorder="little")
-    assert not full[:, :, K:].any()
+    assert not unpack_layers_full(buf, L, R, K)[:, :, K:].any()
 
 
 def test_packer_clip_and_degenerate(pb, orc):

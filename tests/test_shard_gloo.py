@@ -51,8 +51,8 @@ def _worker(rank, world, port, R, K, L, B, a, q):
         codes_full, s_full, _, _ = oracle.quantize_weights(W, L, "grid")
         assert step == s_full and d.scale == s_full
         kw = d.kwords
-        bits = np.unpackbits(buf.reshape(L, rs, kw).view(np.uint8).reshape(L, rs, kw * 4), axis=-1,
-                             bitorder="little")[:, :nr, :K]
+        from packed_layout import unpack_layers
+        bits = unpack_layers(buf, L, rs, K, kw)[:, :nr]
         assert np.array_equal(bits, oracle.decompose(codes_full[r0:r0 + nr], L))
         # shard result (oracle stands in for the GPU), padded to rs rows, gathered
         codes_sh = np.zeros((rs, K), np.int32)
