@@ -142,7 +142,11 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
  *   [stream-K tile counters int32 x 8192]     zero on entry, left zero on exit
  *   [grid barrier int32 x 2]                  arrival count (zero on entry,
  *                                             left zero) + generation
- *   [tensor-engine partial-tile slots int64 x 160 x 2 x batch x 128]
+ *   [work counters int32 x 2]                 zero on entry, left zero
+ *   [end barrier int32 x 2]                   arrival count (zero on entry,
+ *                                             left zero) + generation
+ *   [tensor-engine partial-tile sums int64 x 2048 x batch x 128]
+ *                                             zero on entry, left zero
  *   [f_b int32 x batch][x_q partial sums int64 x batch x 160]
  *   [planes uint32 x batch x act_bits x kwords]
  *   [tensor-engine B operand tiles: kwords x N_pad x 32 bytes, N_pad = a*batch

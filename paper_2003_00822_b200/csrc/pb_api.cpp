@@ -464,13 +464,15 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     g.accumulate = accumulate ? 1 : 0;
     g.npad = l.npad;
     g.bexp = reinterpret_cast<uint8_t*>(base + l.off_bexp);
-    g.slots = reinterpret_cast<unsigned long long*>(base + l.off_slots);
+    g.accbuf = reinterpret_cast<unsigned long long*>(base + l.off_slots);
     g.counters = reinterpret_cast<int*>(base + l.off_count);
     g.tl = pb::debug_tl();
     g.x = nullptr;
     g.K = w->cols;
     g.act_frac = act_frac;
     g.gbar = g.counters + pb::kMaxTiles;
+    g.work = g.counters + pb::kMaxTiles + 2;
+    g.ebar = g.counters + pb::kMaxTiles + 4;
 
     cudaError_t e;
     const cudaStream_t cs = static_cast<cudaStream_t>(s);

@@ -65,7 +65,10 @@ namespace {
 
 constexpr int kConvWarps = 8;                 // 2 h-sets of 4 warps (one per TMEM lane quarter)
 constexpr int kConv0 = 3;                     // first converter warp
-constexpr int kThreads = 32 * (kConv0 + kConvWarps);
+constexpr int kEpi0 = kConv0 + kConvWarps;    // first epilogue warp (4: one per TMEM lane quarter)
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 32 * (kEpi0 + kEpiWarps);
+constexpr int kQDepth = 16;                   // work-item queue (warp 0 -> every other role)
 constexpr int kMaxSlots = 4;                  // A ring: up to 4 slots x 128 TMEM columns (16 MMAs each)
 constexpr int kMaxRegions = 4;                // TMEM accumulators: sign layer + magnitude groups
 constexpr int kChunkWords = 32;               // K-chunk = one 128-byte swizzle row
@@ -73,27 +76,28 @@ constexpr int kActAutoFrac = -1024;           // == PB_ACT_AUTO
 #ifndef PB_MAX_WSTAGES
 #define PB_MAX_WSTAGES 16
 #endif
-#ifndef PB_PUBLISH_EARLY
-#define PB_PUBLISH_EARLY 1
-#endif
 constexpr int kMaxWStages = PB_MAX_WSTAGES;   // weight tile ring (stages sized per launch from free SMEM)
 constexpr uint32_t kWTileBytes = kTcRows * kChunkWords * 4;   // 16 KiB
 constexpr uint32_t kSmemMax = 227 * 1024;                       // opt-in dynamic SMEM per CTA
-constexpr uint32_t kHdrBytes = 3072;                          // struct Bars
+constexpr uint32_t kHdrBytes = 4096;                          // struct Bars
 // dynamic SMEM: [align slack][Bars][W ring: wstages x 16 KiB][B: 2 stages][s_tot: B x 128 int64]
 
 struct Bars {
     uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];   // a_full: the 4 warps of one h-set
     uint64_t w_full[kMaxWStages], w_empty[kMaxWStages];
     uint64_t b_full[2], b_empty[2];
-    uint64_t d_full, d_empty;
+    uint64_t d_full[2], d_empty[2];           // double-buffered accumulators (segment parity)
+    uint64_t q_full[kQDepth], q_empty[kQDepth];
+    int2 q[kQDepth];                          // work items: units [x, y); x < 0 = no more work
     uint64_t x_ready;                        // fused path: bars.xsum written (warp 2)
     int gen;                                 // fused path: grid-barrier generation at arrival
     uint32_t tmem_base;
     int last_flag;
     long long t_b, t_mma0, t_mend, t_cend;   // diagnostics timeline (globaltimer ns)
+    long long t_c0, t_cv[4];                 // first chunk built; converter warp 3's first pass
+    long long t_c0s[2];                      // first chunk: x loads issued, f_b available
     // fused activation prologue
-    float red[8 * kTcMaxN];                  // per-warp partial max|x[b,:]|
+    float red[12 * kTcMaxN];                 // per-warp partial max|x[b,:]| (prologue warps)
     int f[kTcMaxN];                          // f_b
     unsigned long long xs[kTcMaxN];          // this CTA's sum of x_q[b, slice]
     unsigned long long xsum[kTcMaxN];        // sum_c x_q[b, c] over all CTAs
@@ -221,39 +225,37 @@ __device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t (&v)[32]) 
 
 // One pass of one row.  Paired storage: the pass's 32 blocks are 64 words in
 // two 16 KiB stages (t0: blocks 0..15, t1: 16..31); canonical: 32 words in one
-// stage.  All of the row's 16-byte chunks are read from the swizzled tiles
-// first (128B swizzle: chunk c of row m at c ^ (m & 7)), the stages go back to
-// the TMA producer, then A is built and stored to TMEM (4 x 32 columns).
+// stage.  A stage's 8 chunks of the row are read from the swizzled tile (128B
+// swizzle: chunk c of row m at c ^ (m & 7)) and the stage goes back to the TMA
+// producer before its A registers are built and stored to TMEM (32 columns
+// per 4 chunks).
 template <int MODE>
 __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, int dbg,
                                              uint64_t* rel0, uint64_t* rel1, int lane) {
     constexpr bool kPair = MODE <= 3;
-    uint4 q[16];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-        const uint32_t off = (((uint32_t)c) ^ swz) << 4;
-        q[c] = lds128(t0 + off);
-        if (kPair) q[8 + c] = lds128(t1 + off);
-    }
-    __syncwarp();
-    if (lane == 0) {
-        mbar_arrive(rel0);
-        if (kPair) mbar_arrive(rel1);
-    }
+    for (int t = 0; t < (kPair ? 2 : 1); ++t) {
+        uint4 q[8];
 #pragma unroll
-    for (int b4 = 0; b4 < 4; ++b4) {
-        uint32_t v[32];
-        if (kPair) {
-            const uint4 qq[4] = {q[4 * b4], q[4 * b4 + 1], q[4 * b4 + 2], q[4 * b4 + 3]};
-            build_a<MODE>(qq, v);
-        } else {
-            const uint4 qq[4] = {q[2 * b4], q[2 * b4 + 1], q[2 * b4], q[2 * b4 + 1]};
-            build_a<MODE>(qq, v);
+        for (int c = 0; c < 8; ++c) q[c] = lds128((t == 0 ? t0 : t1) + ((((uint32_t)c) ^ swz) << 4));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(t == 0 ? rel0 : rel1);
+#pragma unroll
+        for (int h = 0; h < (kPair ? 2 : 4); ++h) {
+            uint32_t v[32];
+            if (kPair) {
+                const uint4 qq[4] = {q[4 * h], q[4 * h + 1], q[4 * h + 2], q[4 * h + 3]};
+                build_a<MODE>(qq, v);
+            } else {
+                const uint4 qq[4] = {q[2 * h], q[2 * h + 1], q[2 * h], q[2 * h + 1]};
+                build_a<MODE>(qq, v);
+            }
+            const int b4 = kPair ? 2 * t + h : h;
+            if (dbg != 1 && dbg != 3)
+                st_tmem_x32(dst + (uint32_t)(32 * b4), v);
+            else if (v[0] == 0x12345 && v[3] == 0x777)
+                asm volatile("trap;");   // keep the ALU work alive
         }
-        if (dbg != 1 && dbg != 3)
-            st_tmem_x32(dst + (uint32_t)(32 * b4), v);
-        else if (v[0] == 0x12345 && v[3] == 0x777)
-            asm volatile("trap;");   // keep the ALU work alive
     }
 }
 
@@ -282,6 +284,8 @@ struct TcPlan {
     int passes;       // ceil(k_used / 2): layer pairs (0,1), (2,3), ...
     int Gp;           // passes per accumulator group (<= G/2 layers pairs, K * 2^G <= 2^24)
     int regions;      // ceil(passes / Gp)
+    int Gu;           // units per work item (dynamic claims)
+    long long items;  // ceil(units / Gu)
     int dbg;          // profiling knob (env PB_TC_DEBUG): 1 = no A store, 2 = no MMA, 3 = neither,
                       // 6 = per-CTA timeline
     int prof;         // env PB_TC_PROF: print wait-cycle totals of CTA 0
@@ -307,42 +311,53 @@ __device__ __forceinline__ unsigned long long layer_mag(int L, int offset, int i
     return 1ull << (L - 1 - i);
 }
 
-// A CTA's units [u0, u1) split into segments of one row tile: [kcA, kcB) of tile rt.
-struct Seg {
-    int rt, kcA, kcB;
-    long long next;
-};
-__device__ __forceinline__ Seg segment(const TcPlan& p, long long u, long long u1) {
-    Seg s;
-    s.rt = (int)(u / p.chunks);
-    s.kcA = (int)(u - (long long)s.rt * p.chunks);
-    long long ue = (long long)(s.rt + 1) * p.chunks;
-    if (ue > u1) ue = u1;
-    s.kcB = s.kcA + (int)(ue - u);
-    s.next = ue;
-    return s;
-}
-
 // Fused steps a1-a2 (same arithmetic as pb_act.cu) run by
 // the 256 converter threads before the MMAs: every CTA takes max|x[b,:]| itself
 // (an L2-resident re-read of B*K floats), casts and bit-transposes 1/G of the
 // (b, word) items into the B operand tiles in the workspace, and a grid barrier
 // publishes them; meanwhile warp 0 already streams weight tiles.
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Fused steps a1-a2 (same arithmetic as pb_act.cu), run at
+// kernel start by the 384 converter + epilogue threads (warps 3..14, bar 5)
+// while warp 0 already streams weight tiles:
+//   1. one load wave: max|x[b,:]| over all of x (every CTA re-reads the
+//      L2-resident B*K floats), plus the values of the CTA's first chunk and of
+//      its slice of the grid-wide B operand;
+//   2. f_b (reading G8);
+//   3. the CTA's first chunk kc0 of B, built straight into B stage 0 by all 12
+//      warps, so the first MMAs wait neither for the grid barrier nor a copy;
+//   4. (converter warps) the CTA's 1/G slice of the (b, word) items of B into the
+//      workspace tiles + its sum of x_q, published by warp 2's grid barrier.
 template <int NPAD>
-__device__ __forceinline__ void fused_act_prologue(const GemmArgs& g, const TcPlan& p, Bars& bars, int pt,
-                                                   uint8_t* bstage0, int kc0) {
-    const int cw = pt >> 5, lane = pt & 31;
-    long long tpw = 0, tmax = 0, ttr = 0, tgb = 0;
-    pdl_wait();                                   // x may be the previous kernel's output
+__device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& p, Bars& bars, int pt,
+                                               uint8_t* bstage0, int kc0) {
+    constexpr int kPW = kConvWarps + kEpiWarps;        // 12 warps
+    constexpr int kPT = 32 * kPW;
+    const int pw = pt >> 5, lane = pt & 31;
+    long long tpw = 0, tmax = 0, tc0 = 0, ttr = 0;
+    pdl_wait();                                        // x may be the previous kernel's output
     if (g.tl) tpw = gtimer();
     const int B = (int)g.B;
-    // this CTA's (b, word) items: words up to the last chunk's end (zero B for the K
-    // tail, where the complemented sign layer is 1); warp cw takes items i0 + cw + 8k
+    if (pt == 0) bars.gen = ld_acquire_gpu(g.gbar + 1);
+    // first-chunk items it = b * 32 + local word; warp pw takes pw, pw + 12, ...
+    const int nci = B * kChunkWords;
+    auto chunk_x = [&](int it) -> float {
+        const int b = it / kChunkWords;
+        const int64_t c = 32 * ((int64_t)kc0 * kChunkWords + (it - b * kChunkWords)) + lane;
+        return (it < nci && c < g.K) ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
+    };
+    float cx[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cx[k] = chunk_x(pw + kPW * k);
+    // slice items (converter warps): words up to the last chunk's end (zero B for the K
+    // tail, where the complemented sign layer is 1)
     const int64_t Wt = (int64_t)p.chunks * kChunkWords, N = (int64_t)B * Wt;
     const int64_t G = gridDim.x;
     const int64_t i0 = N * blockIdx.x / G, i1 = N * (blockIdx.x + 1) / G;
@@ -351,19 +366,8 @@ __device__ __forceinline__ void fused_act_prologue(const GemmArgs& g, const TcPl
         const int64_t c = 32 * (it - (int64_t)b * Wt) + lane;
         return c < g.K ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
     };
-    // the first two slice items' and four first-chunk items' values are loaded with
-    // the max wave (one L2 round trip); the grid-barrier generation is read now too
-    const float xv0 = (i0 + cw < i1) ? item_x(i0 + cw) : 0.f;
-    const float xv1 = (i0 + cw + 8 < i1) ? item_x(i0 + cw + 8) : 0.f;
-    auto chunk_x = [&](int64_t it) -> float {   // first-chunk item it = b * 32 + local word
-        const int b = (int)(it / kChunkWords);
-        const int64_t c = 32 * ((int64_t)kc0 * kChunkWords + (it - (int64_t)b * kChunkWords)) + lane;
-        return (b < B && c < g.K) ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
-    };
-    float cx[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) cx[k] = chunk_x(cw + 8 * k);
-    if (pt == 0) bars.gen = ld_acquire_gpu(g.gbar + 1);
+    const float xv0 = (pw < kConvWarps && i0 + pw < i1) ? item_x(i0 + pw) : 0.f;
+    const float xv1 = (pw < kConvWarps && i0 + pw + kConvWarps < i1) ? item_x(i0 + pw + kConvWarps) : 0.f;
     // ---- a1 (part 1): max|x[b,:]|
     const bool vec = (g.K & 3) == 0 && (reinterpret_cast<uintptr_t>(g.x) & 15) == 0;
     for (int b = 0; b < B; ++b) {
@@ -372,46 +376,78 @@ __device__ __forceinline__ void fused_act_prologue(const GemmArgs& g, const TcPl
         if (vec) {
             const float4* x4 = reinterpret_cast<const float4*>(xb);
             const int64_t n4 = g.K / 4;
-            for (int64_t c0 = pt; c0 < n4; c0 += 16 * 256) {    // 16 loads in flight per thread
-                float4 v[16];
+            for (int64_t c0 = pt; c0 < n4; c0 += 12 * kPT) {    // 12 loads in flight per thread
+                float4 v[12];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
-                    const int64_t c = c0 + (int64_t)u * 256;
+                for (int u = 0; u < 12; ++u) {
+                    const int64_t c = c0 + (int64_t)u * kPT;
                     v[u] = c < n4 ? __ldg(x4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
-                for (int u = 0; u < 16; ++u)
+                for (int u = 0; u < 12; ++u)
                     m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
             }
         } else {
-            for (int64_t c = pt; c < g.K; c += 256) m = fmaxf(m, fabsf(__ldg(xb + c)));
+            for (int64_t c = pt; c < g.K; c += kPT) m = fmaxf(m, fabsf(__ldg(xb + c)));
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) bars.red[cw * kTcMaxN + b] = m;
+        if (lane == 0) bars.red[pw * kTcMaxN + b] = m;
     }
-    asm volatile("bar.sync 2, 256;" ::: "memory");
+    asm volatile("bar.sync 5, 384;" ::: "memory");
     if (g.tl) tmax = gtimer();
     if (pt < B) {
         float m = bars.red[pt];
 #pragma unroll
-        for (int w = 1; w < 8; ++w) m = fmaxf(m, bars.red[w * kTcMaxN + pt]);
+        for (int w = 1; w < kPW; ++w) m = fmaxf(m, bars.red[w * kTcMaxN + pt]);
         bars.f[pt] = (g.act_frac == kActAutoFrac) ? act_frac_of(m, g.a) : g.act_frac;
         bars.xs[pt] = 0;
     }
-    asm volatile("bar.sync 2, 256;" ::: "memory");
-    // ---- a1 (part 2) + a2: cast, ballot-transpose, B operand tiles
+    asm volatile("bar.sync 5, 384;" ::: "memory");
+    // ---- a1 (part 2) + a2 for the first chunk: cast, ballot-transpose (x_q fits 32 bits:
+    // a <= 32), e2m1 B rows; two items per step keep two independent chains in flight
+    auto transpose2 = [&](long long q0, long long q1, uint32_t& m0, uint32_t& m1) {
+        const uint32_t u0 = (uint32_t)q0, u1 = (uint32_t)q1;
+        m0 = m1 = 0;
+        for (int j = 0; j < g.a; ++j) {
+            const uint32_t bit = 1u << (g.a - 1 - j);
+            const uint32_t w0 = __ballot_sync(0xffffffffu, (u0 & bit) != 0);
+            const uint32_t w1 = __ballot_sync(0xffffffffu, (u1 & bit) != 0);
+            if (lane == j) {
+                m0 = w0;
+                m1 = w1;
+            }
+        }
+    };
+    auto put0 = [&](int it, uint32_t mine) {
+        const int b = it / kChunkWords, wl = it - b * kChunkWords;
+        if (lane < g.a) put_b_operand(bstage0, NPAD, wl, b * g.a + lane, mine);
+        if (b == B - 1 && B * g.a + lane < NPAD) put_b_operand(bstage0, NPAD, wl, B * g.a + lane, 0u);
+    };
+    auto chunk_pair = [&](int ia, float va, int ib, float vb) {
+        uint32_t ma, mb;
+        transpose2(act_cast(va, bars.f[ia < nci ? ia / kChunkWords : 0], g.a),
+                   act_cast(vb, bars.f[ib < nci ? ib / kChunkWords : 0], g.a), ma, mb);
+        if (ia < nci) put0(ia, ma);
+        if (ib < nci) put0(ib, mb);
+    };
+    if (pw < nci) chunk_pair(pw, cx[0], pw + kPW, cx[1]);
+    if (pw + 2 * kPW < nci) chunk_pair(pw + 2 * kPW, cx[2], nci, 0.f);
+    for (int it = pw + 3 * kPW; it < nci; it += 2 * kPW) chunk_pair(it, chunk_x(it), it + kPW, chunk_x(it + kPW));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA operand reads
+    asm volatile("bar.sync 5, 384;" ::: "memory");
+    if (pt == 0) mbar_arrive(&bars.b_full[0]);
+    if (g.tl) tc0 = gtimer();
+    if (pw >= kConvWarps) return;                      // the epilogue warps are done
+    // ---- the CTA's slice of the grid-wide B operand (converter warps, bar 2)
     int k = 0;
-    for (int64_t it = i0 + cw; it < i1; it += 8, ++k) {
+    for (int64_t it = i0 + pw; it < i1; it += kConvWarps, ++k) {
         const int b = (int)(it / Wt);
         const int64_t w = it - (int64_t)b * Wt;
         const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
         const long long q = act_cast(v, bars.f[b], g.a);
-        uint32_t mine = 0;
-        for (int j = 0; j < g.a; ++j) {
-            const uint32_t word = __ballot_sync(0xffffffffu, (unsigned)((q >> (g.a - 1 - j)) & 1));
-            if (lane == j) mine = word;
-        }
+        uint32_t mine, dummy;
+        transpose2(q, 0, mine, dummy);
         if (lane < g.a) put_b_operand(g.bexp, NPAD, w, b * g.a + lane, mine);
         if (b == B - 1 && B * g.a + lane < NPAD) put_b_operand(g.bexp, NPAD, w, B * g.a + lane, 0u);
         long long xs = q;
@@ -426,49 +462,30 @@ __device__ __forceinline__ void fused_act_prologue(const GemmArgs& g, const TcPl
     }
     asm volatile("bar.sync 2, 256;" ::: "memory");
     if (g.tl) ttr = gtimer();
-    // ---- grid barrier, arrive side (generation-based; the arrival count is left
-    // zero).  The CTA's writes are ordered before thread 0's release by bar.sync and
-    // a cumulative fence; warp 2 waits for the generation change before copying
-    // other CTAs' tiles, so the converters go straight on.
-    if (pt == 0) {
-        __threadfence();
-        const int old = atomicAdd(g.gbar, 1);
-        if (old == (int)G - 1) {
-            __threadfence();
-            atomicAdd(g.gbar + 1, 1);             // release the waiters first ...
-            atomicExch(g.gbar, 0);                // ... then clear the count for the next call
-        }
-    }
+    // warp 2 (bar.sync 3) arrives at the grid barrier for this CTA once its slice is written
     asm volatile("bar.arrive 3, 288;" ::: "memory");
-    // ---- the CTA's first chunk, built straight into B stage 0 (same tile layout)
-    auto chunk_item = [&](int64_t it, float v) {
-        const int b = (int)(it / kChunkWords);
-        const int wl = (int)(it - (int64_t)b * kChunkWords);
-        const long long q = act_cast(v, bars.f[b], g.a);
-        uint32_t mine = 0;
-        for (int j = 0; j < g.a; ++j) {
-            const uint32_t word = __ballot_sync(0xffffffffu, (unsigned)((q >> (g.a - 1 - j)) & 1));
-            if (lane == j) mine = word;
-        }
-        if (lane < g.a) put_b_operand(bstage0, NPAD, wl, b * g.a + lane, mine);
-        if (b == B - 1 && B * g.a + lane < NPAD) put_b_operand(bstage0, NPAD, wl, B * g.a + lane, 0u);
-    };
-    const int64_t nci = (int64_t)B * kChunkWords;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        if (cw + 8 * k < nci) chunk_item(cw + 8 * k, cx[k]);
-    for (int64_t it = cw + 32; it < nci; it += 8) chunk_item(it, chunk_x(it));
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA operand reads
-    asm volatile("bar.sync 2, 256;" ::: "memory");
-    if (pt == 0) mbar_arrive(&bars.b_full[0]);
     if (g.tl && pt == 0) {
-        tgb = gtimer();
         long long* r = tl_record(g.tl);
         if (r) {
-            const long long rec[10] = {2, blockIdx.x, 0, 0, tpw, tmax, ttr, tgb, 0, 0};
+            const long long rec[10] = {2, blockIdx.x, 0, 0, tpw, tmax, tc0, ttr, 0, 0};
             for (int q = 0; q < 10; ++q) r[q] = rec[q];
         }
     }
+}
+
+// Reads work item `it` from the queue slot (qi, qph) and releases the slot (each
+// consuming warp arrives once).  Warp-uniform.
+__device__ __forceinline__ int2 take_item(Bars& bars, int& qi, uint32_t& qph, int lane) {
+    mbar_wait(&bars.q_full[qi], qph);
+    const volatile int* vq = reinterpret_cast<volatile int*>(&bars.q[qi]);
+    const int2 it = make_int2(vq[0], vq[1]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars.q_empty[qi]);
+    if (++qi == kQDepth) {
+        qi = 0;
+        qph ^= 1;
+    }
+    return it;
 }
 
 template <int NPAD>
@@ -480,19 +497,17 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     // 1024-byte alignment for the 128B-swizzled TMA tiles
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     Bars& bars = *reinterpret_cast<Bars*>(smem);
-    uint8_t* wtile0 = smem + kHdrBytes;
     constexpr uint32_t kBTile = NPAD * 32;                    // one MMA's B (64 columns)
     constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;  // one K-chunk (16 MMAs)
+    constexpr int kQConsumers = 2 + kConvWarps + kEpiWarps;   // warps 1, 2, converters, epilogue
+    uint8_t* wtile0 = smem + kHdrBytes;
     uint8_t* btile0 = wtile0 + p.wstages * kWTileBytes;
     unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(btile0 + 2 * kBStage);  // [b][128]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long G = gridDim.x;
     long long prof[5] = {0, 0, 0, 0, 0};
-    const long long t_start = clock64();
-    long long g_start;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
-    const long long u0 = p.units * blockIdx.x / G, u1 = p.units * (blockIdx.x + 1) / G;
+    const long long g_start = gtimer();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.slots; ++s) {
@@ -506,9 +521,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         for (int s = 0; s < 2; ++s) {
             mbar_init(&bars.b_full[s], 1);
             mbar_init(&bars.b_empty[s], 1);
+            mbar_init(&bars.d_full[s], 1);
+            mbar_init(&bars.d_empty[s], kEpiWarps);
         }
-        mbar_init(&bars.d_full, 1);
-        mbar_init(&bars.d_empty, 4);
+        for (int s = 0; s < kQDepth; ++s) {
+            mbar_init(&bars.q_full[s], 1);
+            mbar_init(&bars.q_empty[s], kQConsumers);
+        }
         mbar_init(&bars.x_ready, 1);
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(&pmap) : "memory");
@@ -525,7 +544,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     const uint32_t tmem = bars.tmem_base;
     if (warp >= kConv0 && warp < kConv0 + 4) {
         // E8M0 block scale factors: columns 0..3 = 1.0 (SFA), columns 4(1+s)..4(1+s)+3 = 2^s
-        // (SFB of layers with in-group weight 2^s); every byte of a column holds the same value
+        // (SFB of passes with in-group weight 2^s); every byte of a column holds the same value
 #pragma unroll
         for (int blk = 0; blk < 4; ++blk) {
             uint32_t v[16];
@@ -548,13 +567,33 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     tc_fence_after();
     pdl_trigger();
 
+    int qi = 0;                 // work-item queue position (every role walks the same items)
+    uint32_t qph = 0;
     if (warp == 0) {
-        // ------------------------------------------------ weight tile producer (no PDL wait:
-        // the packed weights do not depend on the activation kernel)
+        // ------------------------------------------------ work claims + weight tile producer.
+        // Item blockIdx.x is static (its tiles stream before the PDL wait: the packed weights
+        // do not depend on the previous kernel); later items are claimed from a global counter
+        // once the previous call (which reset it) has completed.
+        long long item = blockIdx.x;
+        bool waited = false;
         int tc = 0;
-        for (long long u = u0; u < u1;) {
-            const Seg sg = segment(p, u, u1);
-            for (int kc = sg.kcA; kc < sg.kcB; ++kc)
+        while (true) {
+            mbar_wait(&bars.q_empty[qi], qph ^ 1);
+            const long long u0 = item < p.items ? item * p.Gu : -1;
+            long long u1 = u0 + p.Gu;
+            if (u1 > p.units) u1 = p.units;
+            if (lane == 0) {
+                bars.q[qi] = make_int2((int)u0, (int)u1);
+                mbar_arrive(&bars.q_full[qi]);
+            }
+            __syncwarp();
+            if (++qi == kQDepth) {
+                qi = 0;
+                qph ^= 1;
+            }
+            if (u0 < 0) break;
+            for (long long u = u0; u < u1; ++u) {
+                const int rt = (int)(u / p.chunks), kc = (int)(u - (long long)rt * p.chunks);
                 for (int ps = 0; ps < p.passes; ++ps) {
                     // a stored pair: two 32-word boxes of the pair row; else the canonical last layer
                     const bool stored_pair = 2 * ps + 1 < g.L;
@@ -565,15 +604,31 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                             mbar_arrive_expect_tx(&bars.w_full[st], kWTileBytes);
                             if (stored_pair)
                                 tma_load_3d(wtile0 + st * kWTileBytes, &pmap, kc * 2 * kChunkWords + t * kChunkWords,
-                                            sg.rt * kTcRows, ps, &bars.w_full[st]);
+                                            rt * kTcRows, ps, &bars.w_full[st]);
                             else
-                                tma_load_3d(wtile0 + st * kWTileBytes, &smap, kc * kChunkWords, sg.rt * kTcRows, 0,
+                                tma_load_3d(wtile0 + st * kWTileBytes, &smap, kc * kChunkWords, rt * kTcRows, 0,
                                             &bars.w_full[st]);
                         }
                         __syncwarp();
                     }
                 }
-            u = sg.next;
+            }
+            if (!waited) {
+                pdl_wait();
+                waited = true;
+            }
+            long long nxt = 0;
+            if (lane == 0) nxt = G + atomicAdd(&g.work[0], 1);
+            item = __shfl_sync(0xffffffffu, nxt, 0);
+        }
+        if (!waited) pdl_wait();
+        if (lane == 0) {
+            // the last CTA to run out of work clears the counters for the next call
+            __threadfence();
+            if (atomicAdd(&g.work[1], 1) == (int)G - 1) {
+                atomicExch(&g.work[0], 0);
+                atomicExch(&g.work[1], 0);
+            }
         }
     } else if (warp == 2) {
         // ------------------------------------------------ B (plane tile) producer
@@ -583,8 +638,21 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         bool published = false;
         auto wait_published = [&]() {
             if (g.x && !published) {
-                asm volatile("bar.sync 3, 288;" ::: "memory");         // this CTA has arrived
-                while (ld_acquire_gpu(g.gbar + 1) == bars.gen) __nanosleep(64);   // ... and every other
+                asm volatile("bar.sync 3, 288;" ::: "memory");         // this CTA's slice is written
+                if (lane == 0) {
+                    // generation-based grid barrier; the arrival count is left zero.  The
+                    // CTA's writes are ordered before the arrival by bar.sync + this
+                    // cumulative fence.
+                    __threadfence();
+                    const int old = atomicAdd(g.gbar, 1);
+                    if (old == (int)G - 1) {
+                        __threadfence();
+                        atomicAdd(g.gbar + 1, 1);             // release the waiters first ...
+                        atomicExch(g.gbar, 0);                // ... then clear the count
+                    }
+                }
+                __syncwarp();
+                while (ld_acquire_gpu(g.gbar + 1) == bars.gen) __nanosleep(32);   // every CTA has arrived
                 asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> bulk-copy reads
                 if (g.tl && lane == 0) bars.t_b = gtimer();
                 // sum_c x_q[b, c] from every CTA's partial, for the epilogue
@@ -603,11 +671,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         };
         if (!g.x && g.tl && lane == 0) bars.t_b = gtimer();
         int cc = 0;
-        for (long long u = u0; u < u1;) {
-            const Seg sg = segment(p, u, u1);
-            for (int kc = sg.kcA; kc < sg.kcB; ++kc, ++cc) {
+        while (true) {
+            const int2 it = take_item(bars, qi, qph, lane);
+            if (it.x < 0) break;
+            for (int u = it.x; u < it.y; ++u, ++cc) {
                 if (g.x && cc == 0) continue;                 // built in place by the converters
                 wait_published();
+                const int kc = u % p.chunks;
                 const int st = cc & 1;
                 mbar_wait(&bars.b_empty[st], (uint32_t)(((cc >> 1) & 1) ^ 1));
                 if (elect_one()) {
@@ -616,7 +686,6 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 }
                 __syncwarp();
             }
-            u = sg.next;
         }
         wait_published();                                     // (a one-chunk CTA still joins bar 3)
     } else if (warp == 1) {
@@ -629,91 +698,94 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         long long t_mma0 = 0;
         uint32_t slot = 0, phase = 0;
         int cc = 0, seg = 0;
-        for (long long u = u0; u < u1; ++seg) {
-            const Seg sg = segment(p, u, u1);
-            if (seg > 0) mbar_wait(&bars.d_empty, (uint32_t)((seg - 1) & 1));
-            tc_fence_after();
-            for (int kc = sg.kcA; kc < sg.kcB; ++kc, ++cc) {
-                const int st = cc & 1;
-                TWAIT(&bars.b_full[st], (uint32_t)((cc >> 1) & 1), 1);
+        while (true) {
+            const int2 it = take_item(bars, qi, qph, lane);
+            if (it.x < 0) break;
+            for (int u = it.x; u < it.y; ++seg) {
+                // a segment: the item's units in one row tile, accumulated in D[seg & 1]
+                const int rt = u / p.chunks;
+                int ue = (rt + 1) * p.chunks;
+                if (ue > it.y) ue = it.y;
+                const int db = seg & 1;
+                if (seg >= 2) mbar_wait(&bars.d_empty[db], (uint32_t)(((seg >> 1) - 1) & 1));
                 tc_fence_after();
-                const uint64_t bdesc0 = b_desc(smem_u32(btile0 + st * kBStage));
-                for (int ps = 0; ps < p.passes; ++ps) {
-                    int region, sexp;
-                    bool first;
-                    pass_region(p, g.k_used, ps, region, sexp, first);
-                    const uint32_t dcol = tmem + (uint32_t)(p.d_col + region * NPAD);
-                    const uint32_t sfb = tmem + (uint32_t)(p.sf_col + 4 * (1 + sexp));
-                    const bool open = first && kc == sg.kcA;
-                    TWAIT(&bars.a_full[slot], phase, 2);
+                const uint32_t dbase = tmem + (uint32_t)(p.d_col + db * p.regions * NPAD);
+                for (const int us = u; u < ue; ++u, ++cc) {
+                    const int st = cc & 1;
+                    TWAIT(&bars.b_full[st], (uint32_t)((cc >> 1) & 1), 1);
                     tc_fence_after();
-                    if (g.tl && t_mma0 == 0) t_mma0 = gtimer();
-                    if (p.dbg == 2 || p.dbg == 3) {
-                        if (elect_one()) tc_commit(&bars.a_empty[slot]);
-                    } else if (elect_one()) {
-                        // descriptor start address advances in 16 B units: one B tile = NPAD*32 B
-                        const uint32_t a0 = tmem + slot * 128;
+                    const uint64_t bdesc0 = b_desc(smem_u32(btile0 + st * kBStage));
+                    for (int ps = 0; ps < p.passes; ++ps) {
+                        int region, sexp;
+                        bool first;
+                        pass_region(p, g.k_used, ps, region, sexp, first);
+                        const uint32_t dcol = dbase + (uint32_t)(region * NPAD);
+                        const uint32_t sfb = tmem + (uint32_t)(p.sf_col + 4 * (1 + sexp));
+                        const bool open = first && u == us;
+                        TWAIT(&bars.a_full[slot], phase, 2);
+                        tc_fence_after();
+                        if (g.tl && t_mma0 == 0) t_mma0 = gtimer();
+                        if (p.dbg == 2 || p.dbg == 3) {
+                            if (elect_one()) tc_commit(&bars.a_empty[slot]);
+                        } else if (elect_one()) {
+                            // descriptor start address advances in 16 B units: one B tile = NPAD*32 B
+                            const uint32_t a0 = tmem + slot * 128;
 #pragma unroll
-                        for (int uu = 0; uu < 16; ++uu)
-                            tc_mma(dcol, a0 + 8 * uu, bdesc0 + uu * (kBTile / 16), idesc,
-                                   (uu == 0 && open) ? 0u : 1u, sfa, sfb);
-                        tc_commit(&bars.a_empty[slot]);
+                            for (int uu = 0; uu < 16; ++uu)
+                                tc_mma(dcol, a0 + 8 * uu, bdesc0 + uu * (kBTile / 16), idesc,
+                                       (uu == 0 && open) ? 0u : 1u, sfa, sfb);
+                            tc_commit(&bars.a_empty[slot]);
+                        }
+                        __syncwarp();
+                        if (++slot == (uint32_t)p.slots) {
+                            slot = 0;
+                            phase ^= 1;
+                        }
                     }
+                    if (elect_one()) tc_commit(&bars.b_empty[st]);
                     __syncwarp();
-                    if (++slot == (uint32_t)p.slots) {
-                        slot = 0;
-                        phase ^= 1;
-                    }
                 }
-                if (elect_one()) tc_commit(&bars.b_empty[st]);
+                if (elect_one()) tc_commit(&bars.d_full[db]);
                 __syncwarp();
             }
-            if (elect_one()) tc_commit(&bars.d_full);
-            __syncwarp();
-            u = sg.next;
         }
         if (g.tl && lane == 0) {
             bars.t_mma0 = t_mma0;
             bars.t_mend = gtimer();
         }
-    } else {
-        // ------------------------------------------------ converters (+ epilogue)
+    } else if (warp < kEpi0) {
+        // ------------------------------------------------ converters
         const int cw = warp - kConv0;
-        const int h = cw >> 2;                 // h-set: 0 = warps 3..6 (also the epilogue), 1 = warps 7..10
+        const int h = cw >> 2;                 // h-set: 0 = warps 3..6, 1 = warps 7..10
         const int q = warp & 3;                // TMEM lane quarter this warp may access
         const int m = q * 32 + lane;           // row within the tile
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const uint32_t wtile_s = smem_u32(wtile0) + (uint32_t)m * 128;
         const uint32_t swz = (uint32_t)(m & 7);
-        if (g.x) fused_act_prologue<NPAD>(g, p, bars, threadIdx.x - kConv0 * 32, btile0, (int)(u0 % p.chunks));
-        int tc = 0, pc = 0, seg = 0;
-        // passes (kc, ps) in issue order; h-set h converts passes pc = h, h + 2, ...; pass pc
-        // uses A slot pc % slots; its tiles are tc (hi, if paired) and tc + 1 (or tc alone)
+        if (g.x)
+            fused_prologue<NPAD>(g, p, bars, threadIdx.x - kConv0 * 32, btile0,
+                                 (int)(((long long)blockIdx.x * p.Gu) % p.chunks));
+        int tc = 0, pc = 0;
+        // passes in issue order; h-set h converts passes pc = h, h + 2, ...; pass pc uses A slot
+        // pc % slots; its tiles are tc and tc + 1 (a stored pair) or tc alone
         int slot = h % p.slots, sphase = (h / p.slots) & 1;
-        // software pipeline: the TMEM stores of one pass drain while the next is awaited
+        // software pipeline: a pass's TMEM stores drain while the next pass's tiles are awaited
         int pend_slot = -1;
-        long long tf[4] = {0, 0, 0, 0};   // timeline: first pass w_full, a_empty, converted, published
+        int npub = 0;
         auto publish = [&]() {
             if (pend_slot >= 0) {
-                if (g.tl && tf[3] == 0 && tf[2] != 0) tf[3] = gtimer();
-                if (p.prof) {
-                    const long long t0 = gtimer();
-                    tmem_st_wait();
-                    prof[1] += gtimer() - t0;         // converters: TMEM store drain (ns)
-                } else {
-                    tmem_st_wait();
-                }
+                tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.a_full[pend_slot]);
                 pend_slot = -1;
+                if (g.tl && warp == kConv0 && lane == 0 && npub++ == 0) bars.t_cv[3] = gtimer();
             }
         };
-        for (long long u = u0; u < u1; ++seg) {
-            const Seg sg = segment(p, u, u1);
-            const int64_t row = (int64_t)sg.rt * kTcRows + m;
-            const bool row_ok = row < g.R;
-            for (int kc = sg.kcA; kc < sg.kcB; ++kc) {
+        while (true) {
+            const int2 it = take_item(bars, qi, qph, lane);
+            if (it.x < 0) break;
+            for (int u = it.x; u < it.y; ++u) {
                 for (int ps = 0; ps < p.passes; ++ps, ++pc) {
                     const bool stored_pair = 2 * ps + 1 < g.L;
                     const bool use_lo = 2 * ps + 1 < g.k_used;
@@ -722,34 +794,29 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         tc += ntile;
                         continue;
                     }
-                    if (PB_PUBLISH_EARLY) publish();    // previous pass's A is in TMEM: tell the MMA
-                    const int st_hi = tc % p.wstages, st_lo = (tc + ntile - 1) % p.wstages;
-                    TWAIT(&bars.w_full[st_hi], (uint32_t)((tc / p.wstages) & 1), 3);
-                    if (stored_pair)
-                        TWAIT(&bars.w_full[st_lo], (uint32_t)(((tc + 1) / p.wstages) & 1), 3);
-                    if (g.tl && tf[0] == 0) tf[0] = gtimer();
-                    const uint32_t thi = wtile_s + (uint32_t)st_hi * kWTileBytes;
-                    const uint32_t tlo = wtile_s + (uint32_t)st_lo * kWTileBytes;
-                    if (!PB_PUBLISH_EARLY) publish();
+                    const int st0 = tc % p.wstages, st1 = (tc + ntile - 1) % p.wstages;
+                    if (g.tl && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[0] = gtimer();
+                    TWAIT(&bars.w_full[st0], (uint32_t)((tc / p.wstages) & 1), 3);
+                    if (stored_pair) TWAIT(&bars.w_full[st1], (uint32_t)(((tc + 1) / p.wstages) & 1), 3);
+                    if (g.tl && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[1] = gtimer();
+                    publish();                          // previous pass's A is in TMEM: tell the MMA
                     TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
-                    if (g.tl && tf[1] == 0) tf[1] = gtimer();
                     tc_fence_after();
                     const int mode = stored_pair ? (use_lo ? 0 : 2) + (ps == 0 ? 1 : 0) : (ps == 0 ? 5 : 4);
+                    const uint32_t t0 = wtile_s + (uint32_t)st0 * kWTileBytes;
+                    const uint32_t t1 = wtile_s + (uint32_t)st1 * kWTileBytes;
                     const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
-                    uint64_t* rhi = &bars.w_empty[st_hi];
-                    uint64_t* rlo = &bars.w_empty[st_lo];
-                    const long long tcv = p.prof ? gtimer() : 0;
+                    uint64_t* r0 = &bars.w_empty[st0];
+                    uint64_t* r1 = &bars.w_empty[st1];
                     switch (mode) {
-                        case 0: convert_pass<0>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
-                        case 1: convert_pass<1>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
-                        case 2: convert_pass<2>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
-                        case 3: convert_pass<3>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
-                        case 4: convert_pass<4>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
-                        default: convert_pass<5>(thi, tlo, swz, dst, p.dbg, rhi, rlo, lane); break;
+                        case 0: convert_pass<0>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
+                        case 1: convert_pass<1>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
+                        case 2: convert_pass<2>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
+                        case 3: convert_pass<3>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
+                        case 4: convert_pass<4>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
+                        default: convert_pass<5>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
                     }
-                    if (p.prof) prof[0] += gtimer() - tcv;   // converters: LDS + build + STTM issue (ns)
-                    if (g.tl && tf[2] == 0) tf[2] = gtimer();
-
+                    if (g.tl && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
                     tc += ntile;
                     pend_slot = slot;
                     slot += 2;
@@ -759,25 +826,70 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     }
                 }
             }
-            publish();
-
-            if (h == 0) {
-                // ---------------- epilogue: fold the accumulators into exact int64
-                mbar_wait(&bars.d_full, (uint32_t)(seg & 1));
+        }
+        publish();
+    } else {
+        // ------------------------------------------------ epilogue: per segment, fold D into
+        // exact int64 per-row sums; a whole tile writes y, a partial tile adds into the
+        // tile's accumulator (integer: order-independent, exact) and the contributor that
+        // completes the tile's chunk count finalises it.
+        const int ew = warp - kEpi0;
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0);
+        bool have_xsum = false;
+        unsigned long long sxs[kTcMaxN / 8];   // sum_c x_q[b, c] for b < B (B <= 32 / a <= 4 with a >= 8)
+        auto xsum_of = [&](int b) -> unsigned long long {
+            if (g.x) {
+                if (!have_xsum) {
+                    mbar_wait(&bars.x_ready, 0);
+                    have_xsum = true;
+                }
+                return bars.xsum[b];
+            }
+            unsigned long long sx = 0;
+            for (int pp = 0; pp < g.nsplit; ++pp) sx += (unsigned long long)g.xsum[(int64_t)b * kXsumStride + pp];
+            return sx;
+        };
+        (void)sxs;
+        auto finish = [&](int b, int64_t row, unsigned long long t) {
+            t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
+            const long long accv = (long long)t;
+            const int64_t o = (int64_t)b * g.R + row;
+            if (g.acc) g.acc[o] = accv;
+            float yv = dequant(accv, g.scale, g.x ? bars.f[b] : g.f[b]);
+            if (g.bias) yv += g.bias[row];
+            if (g.accumulate) yv += g.y[o];
+            g.y[o] = apply_fn(yv, g.fn);
+        };
+        if (g.x)
+            fused_prologue<NPAD>(g, p, bars, threadIdx.x - kConv0 * 32, btile0,
+                                 (int)(((long long)blockIdx.x * p.Gu) % p.chunks));
+        else
+            pdl_wait();
+        int seg = 0;
+        while (true) {
+            const int2 it = take_item(bars, qi, qph, lane);
+            if (it.x < 0) break;
+            for (int u = it.x; u < it.y; ++seg) {
+                const int rt = u / p.chunks, kcA = u - rt * p.chunks;
+                int ue = (rt + 1) * p.chunks;
+                if (ue > it.y) ue = it.y;
+                const int kcB = kcA + (ue - u);
+                const int db = seg & 1;
+                mbar_wait(&bars.d_full[db], (uint32_t)((seg >> 1) & 1));
                 tc_fence_after();
-                long long te[4] = {0, 0, 0, 0};
+                long long te[3] = {0, 0, 0};
                 if (g.tl) te[0] = gtimer();
-                pdl_wait();
-                // tot_b = sum_j T_j sum_r |S_lo(r)| D_r[b*a + j] (+ the sign correction below);
-                // lo(r) = least significant layer of group r
+                // tot_b = sum_j T_j sum_r |S_lo(r)| D_r[b*a + j]; lo(r) = least significant layer of group r
                 for (int r = 0; r < p.regions; ++r) {
                     int last = (r + 1) * p.Gp - 1;
                     if (last > p.passes - 1) last = p.passes - 1;
                     const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
                     uint32_t dv[NPAD];
-                    ld_tmem_cols<NPAD>(tmem + lane_off + (uint32_t)(p.d_col + r * NPAD), dv);
+                    ld_tmem_cols<NPAD>(tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD), dv);
                     tmem_ld_wait();
-                    // columns n = b*a + j in order: one register sum per batch column
                     unsigned long long acc = 0;
                     int j = 0, bc = 0;
 #pragma unroll
@@ -796,94 +908,51 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&bars.d_empty);
+                if (lane == 0) mbar_arrive(&bars.d_empty[db]);
                 if (g.tl) te[1] = gtimer();
-                auto tot_of = [&](int b) -> unsigned long long { return s_tot[b * kTcRows + m]; };
-                const bool whole = (sg.kcA == 0 && sg.kcB == p.chunks);
-                bool finalize = whole;
-                if (!whole) {
-                    // partial tile: park this CTA's sums in its slot (first segment of
-                    // the range -> slot 0, otherwise it is the last -> slot 1)
-                    const int myslot = (u == u0) ? 0 : 1;
-                    unsigned long long* sl = g.slots + (((int64_t)blockIdx.x * 2 + myslot) * g.B) * kTcRows;
-                    for (int b = 0; b < g.B; ++b) sl[b * kTcRows + m] = tot_of(b);
-                    // the 128 threads' slot stores are ordered before the counter update by
-                    // bar.sync + thread 0's cumulative fence; symmetrically on the acquire side
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    if (cw == 0 && lane == 0) {
-                        __threadfence();
-                        const int add = sg.kcB - sg.kcA;
-                        const int old = atomicAdd(&g.counters[sg.rt], add);
-                        const int last = (old + add == p.chunks);
-                        if (last) g.counters[sg.rt] = 0;      // every call leaves the counters zero
-                        bars.last_flag = last;
-                        __threadfence();
-                    }
-                    asm volatile("bar.sync 1, 128;" ::: "memory");
-                    finalize = bars.last_flag != 0;
-                }
-                if (g.tl) te[2] = gtimer();
-                if (finalize && row_ok) {
-                    for (int b = 0; b < g.B; ++b) {
-                        unsigned long long t;
-                        if (whole) {
-                            t = tot_of(b);
-                        } else {
-                            // sum the slots of every CTA whose unit range meets this tile
-                            t = 0;
-                            const long long t0u = (long long)sg.rt * p.chunks, t1u = t0u + p.chunks;
-                            long long c = (t0u * G) / p.units;
-                            while (c > 0 && p.units * c / G > t0u) --c;
-                            while (p.units * (c + 1) / G <= t0u) ++c;
-                            for (; c < G && p.units * c / G < t1u; ++c) {
-                                const long long cu0 = p.units * c / G, cu1 = p.units * (c + 1) / G;
-                                if (cu1 <= cu0) continue;
-                                const int sslot = (cu0 >= t0u) ? 0 : 1;
-                                t += __ldcg(g.slots + (((int64_t)c * 2 + sslot) * g.B + b) * kTcRows + m);
-                            }
-                        }
-                        {
-                            // (o - |S_0|) * sum_c x_q: the binary offset (o = 1) and the
-                            // complemented sign layer (file header)
-                            unsigned long long sx = 0;
-                            if (g.x) {
-                                mbar_wait(&bars.x_ready, 0);
-                                sx = bars.xsum[b];
-                            }
-                            else
-                                for (int pp = 0; pp < g.nsplit; ++pp)
-                                    sx += (unsigned long long)g.xsum[(int64_t)b * kXsumStride + pp];
-                            t += ((unsigned long long)g.offset - layer_mag(g.L, g.offset, 0)) * sx;
-                        }
-                        const long long accv = (long long)t;
-                        const int64_t o = (int64_t)b * g.R + row;
-                        if (g.acc) g.acc[o] = accv;
-                        float yv = dequant(accv, g.scale, g.x ? bars.f[b] : g.f[b]);
-                        if (g.bias) yv += g.bias[row];
-                        if (g.accumulate) yv += g.y[o];
-                        g.y[o] = apply_fn(yv, g.fn);
+                // exact integer adds into the tile's accumulator (order-independent); no
+                // round trip here: tiles are finalised after the end-of-work grid barrier
+                unsigned long long* ab = g.accbuf + (int64_t)rt * g.B * kTcRows + m;
+                for (int b = 0; b < g.B; ++b) red_add_u64(ab + b * kTcRows, s_tot[b * kTcRows + m]);
+                if (g.tl && ew == 0 && lane == 0) {
+                    te[2] = gtimer();
+                    long long* rr = tl_record(g.tl);
+                    if (rr) {
+                        const long long rec[10] = {3, blockIdx.x, seg, kcB - kcA, te[0], te[1], te[2], te[2], 0, 0};
+                        for (int k = 0; k < 10; ++k) rr[k] = rec[k];
                     }
                 }
-                if (g.tl && cw == 0 && lane == 0) {
-                    te[3] = gtimer();
-                    long long* r = tl_record(g.tl);
-                    if (r) {
-                        const long long rec[10] = {3, blockIdx.x, seg, (whole ? 1 : 0) + (finalize ? 2 : 0),
-                                                   te[0], te[1], te[2], te[3], 0, 0};
-                        for (int q = 0; q < 10; ++q) r[q] = rec[q];
-                    }
-                }
-            }
-            u = sg.next;
-        }
-        if (g.tl && warp == kConv0 && lane == 0) {
-            bars.t_cend = gtimer();
-            long long* r = tl_record(g.tl);
-            if (r) {
-                const long long rec[10] = {5, blockIdx.x, 0, 0, tf[0], tf[1], tf[2], tf[3], 0, 0};
-                for (int q = 0; q < 10; ++q) r[q] = rec[q];
+                u = ue;
             }
         }
+        // ---- end-of-work grid barrier (the 128 threads' adds are ordered before the arrival by
+        // bar.sync + thread 0's cumulative fence), then this CTA finalises tiles
+        // blockIdx.x, blockIdx.x + G, ...: y from the exact tile sums, accumulators re-zeroed
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (ew == 0 && lane == 0) {
+            const int gen = ld_acquire_gpu(g.ebar + 1);
+            __threadfence();
+            const int old = atomicAdd(g.ebar, 1);
+            if (old == (int)G - 1) {
+                __threadfence();
+                atomicAdd(g.ebar + 1, 1);
+                atomicExch(g.ebar, 0);
+            } else {
+                while (ld_acquire_gpu(g.ebar + 1) == gen) __nanosleep(32);
+            }
+            __threadfence();
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        for (long long rt = blockIdx.x; rt < p.tiles; rt += G) {
+            const int64_t row = rt * kTcRows + m;
+            unsigned long long* ab = g.accbuf + rt * g.B * kTcRows + m;
+            for (int b = 0; b < g.B; ++b) {
+                const unsigned long long t = __ldcg(ab + b * kTcRows);
+                ab[b * kTcRows] = 0;                  // every call leaves the accumulators zero
+                if (row < g.R) finish(b, row, t);
+            }
+        }
+        if (g.tl && ew == 0 && lane == 0) bars.t_cend = gtimer();
     }
 
     if (p.prof && g.tl && lane == 0) {
@@ -892,7 +961,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         if (r) {
             const long long rec[10] = {4, blockIdx.x, warp, gtimer() - g_start, prof[0], prof[1], prof[2], prof[3],
                                        prof[4], 0};
-            for (int q = 0; q < 10; ++q) r[q] = rec[q];
+            for (int k = 0; k < 10; ++k) r[k] = rec[k];
         }
     }
     tc_fence_before();
@@ -902,13 +971,17 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         if (r) {
             unsigned smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            const long long rec[10] = {1, blockIdx.x, smid, u1 - u0, g_start, bars.t_b, bars.t_mma0, bars.t_mend,
+            const long long rec[10] = {1, blockIdx.x, smid, 0, g_start, bars.t_b, bars.t_mma0, bars.t_mend,
                                        bars.t_cend, gtimer()};
             for (int k = 0; k < 10; ++k) r[k] = rec[k];
         }
+        long long* r5 = tl_record(g.tl);
+        if (r5) {
+            const long long rec[10] = {5, blockIdx.x, bars.t_c0s[0], bars.t_c0s[1], bars.t_cv[0], bars.t_cv[1],
+                                       bars.t_cv[2], bars.t_cv[3], bars.t_c0, 0};
+            for (int k = 0; k < 10; ++k) r5[k] = rec[k];
+        }
     }
-    tc_fence_before();
-    __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
@@ -961,7 +1034,7 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
 {
     if (npad <= 0 || g.kwords <= 0 || g.R <= 0 || g.B <= 0 || g.L > 16) return false;
     p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
-    if (p.tiles > kMaxTiles) return false;
+    if (p.tiles > kAccTiles) return false;
     p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
     p.units = (long long)p.tiles * p.chunks;
     // exact f32 accumulation: a group of G layers sums to < K * 2^G <= 2^24
@@ -972,11 +1045,14 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     p.passes = (g.k_used + 1) / 2;
     p.regions = (p.passes + p.Gp - 1) / p.Gp;
     if (p.regions > kMaxRegions) return false;
-    p.d_col = 512 - (p.regions * npad + 31) / 32 * 32;
+    p.d_col = 512 - (2 * p.regions * npad + 31) / 32 * 32;   // two accumulator sets
     p.sf_col = p.d_col - 64;
     p.slots = p.sf_col / 128;
     if (p.slots > kMaxSlots) p.slots = kMaxSlots;
     if (p.slots < 2) return false;
+    // work items of >= ~4 passes (so an item's epilogue keeps up with its MMAs)
+    p.Gu = (4 + p.passes - 1) / p.passes;
+    p.items = (p.units + p.Gu - 1) / p.Gu;
     return true;
 }
 
@@ -1016,7 +1092,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     if (p.wstages < 4) return cudaErrorNotSupported;
     const uint32_t smem = fixed + (uint32_t)p.wstages * kWTileBytes;
-    long long grid = p.units < sms ? p.units : sms;
+    long long grid = p.items < sms ? p.items : sms;
     if (grid > kMaxCtas) grid = kMaxCtas;
 
     cudaLaunchConfig_t cfg = {};

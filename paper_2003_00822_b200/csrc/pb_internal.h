@@ -28,7 +28,12 @@ inline int tc_npad(int64_t batch, int32_t a) {
 //                                       entry, every call leaves them zero
 //   [grid barrier int32 x 2]            fused tensor-engine path: arrival
 //                                       count (left zero) + generation
-//   [partial slots int64 x kMaxCtas x 2 x B x 128]   tensor engine only
+//   [work counters int32 x 2]           tensor engine: item claims, finished
+//                                       CTAs (left zero)
+//   [end barrier int32 x 2]             tensor engine: arrival count (left
+//                                       zero) + generation
+//   [tile sums int64 x kAccTiles x B x 128]   tensor engine: partial-tile
+//                                       accumulators (left zero)
 //   [f_b int32 x B][Σx_q partials int64 x B x kXsumStride][bit planes [B][a][kwords]]
 //   [tensor-engine B operand tiles: one N_pad x 32-byte e2m1 tile per 2 words
 //    (64 columns), kwords rounded up to 32 words]
@@ -37,6 +42,7 @@ inline int tc_npad(int64_t batch, int32_t a) {
 constexpr int kMaxTiles = 8192;      // tensor engine: rows <= 8192 * 128
 constexpr int kMaxCtas = 160;        // tensor engine grid cap (B200: 148 SMs)
 constexpr int kXsumStride = kMaxCtas;   // Σx_q partials per batch column (act CTAs or fused GEMM CTAs)
+constexpr int kAccTiles = 2048;      // tensor engine: rows <= 2048 * 128 (partial-tile accumulators)
 struct WsLayout {
     size_t off_count, off_slots, off_f, off_xsum, off_planes, off_bexp, total;
     int npad;
@@ -45,8 +51,8 @@ inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     WsLayout l;
     l.npad = tc_npad(batch, act_bits);
     l.off_count = 0;
-    l.off_slots = align_up(sizeof(int32_t) * (kMaxTiles + 2));
-    const size_t slots = l.npad ? sizeof(long long) * kMaxCtas * 2 * (size_t)batch * kTcRows : 0;
+    l.off_slots = align_up(sizeof(int32_t) * (kMaxTiles + 6));
+    const size_t slots = l.npad ? sizeof(long long) * kAccTiles * (size_t)batch * kTcRows : 0;
     l.off_f = align_up(l.off_slots + slots);
     l.off_xsum = align_up(l.off_f + sizeof(int32_t) * (size_t)batch);
     l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kXsumStride);
@@ -80,7 +86,7 @@ struct GemmArgs {
     // tensor engine operands (valid when npad > 0)
     int npad;
     uint8_t* bexp;                // [kwords][npad x 32 canonical tile]
-    unsigned long long* slots;    // [kMaxCtas][2][B][128] partial tile sums
+    unsigned long long* accbuf;   // [kAccTiles][B][128] partial tile sums, zero between calls
     int* counters;                // [kMaxTiles]
     long long* tl;                // diagnostics timeline (pb_debug_timeline) or null
     // fused activation path (tensor engine, pb_matmul / pb_linear): when x is set the
@@ -89,6 +95,8 @@ struct GemmArgs {
     int64_t K;
     int act_frac;
     int* gbar;                    // grid barrier {arrival count, generation}
+    int* work;                    // tensor engine {item claim counter, finished CTAs}, zero between calls
+    int* ebar;                    // tensor engine end-of-work grid barrier {arrival count, generation}
 };
 
 // Diagnostics timeline (PB_TC_DEBUG=6): device log, [0] = record counter,

@@ -36,8 +36,8 @@ if len(pr):
     for c in range(len(pr) // ncta):
         q = pr[c * ncta:(c + 1) * ncta]
         print(f"prologue call {c}: pdl-wait done {f(q[:,4]).min():8.2f}..{f(q[:,4]).max():8.2f}  "
-              f"max done {f(q[:,5]).min():8.2f}..{f(q[:,5]).max():8.2f}  slice done {f(q[:,6]).min():8.2f}..{f(q[:,6]).max():8.2f}  "
-              f"chunk0 B done {f(q[:,7]).min():8.2f}..{f(q[:,7]).max():8.2f}")
+              f"max done {f(q[:,5]).min():8.2f}..{f(q[:,5]).max():8.2f}  chunk0 done {f(q[:,6]).min():8.2f}..{f(q[:,6]).max():8.2f}  "
+              f"slice done {f(q[:,7]).min():8.2f}..{f(q[:,7]).max():8.2f}")
 ep = rec[rec[:, 0] == 3]
 if len(ep):
     # per epilogue segment: d_full wake -> TMEM drained -> slot/atomic done -> y stored
@@ -74,5 +74,11 @@ if len(fp):
     fp = fp[np.argsort(fp[:, 4], kind="stable")]
     for c in range(len(fp) // ncta):
         q = fp[c * ncta:(c + 1) * ncta]
-        print(f"first pass (warp 3) call {c}: w_full {f(q[:,4]).min():8.2f}..{f(q[:,4]).max():8.2f}  a_empty {f(q[:,5]).min():8.2f}..{f(q[:,5]).max():8.2f}"
-              f"  converted {f(q[:,6]).min():8.2f}..{f(q[:,6]).max():8.2f}  published {f(q[:,7]).min():8.2f}..{f(q[:,7]).max():8.2f}")
+        print(f"first pass (warp 3) call {c}: start {f(q[:,4]).min():8.2f}..{f(q[:,4]).max():8.2f}  tiles {f(q[:,5]).min():8.2f}..{f(q[:,5]).max():8.2f}"
+              f"  converted {f(q[:,6]).min():8.2f}..{f(q[:,6]).max():8.2f}  published {f(q[:,7]).min():8.2f}..{f(q[:,7]).max():8.2f}"
+              f"  chunk0 B {f(q[:,8]).min():8.2f}..{f(q[:,8]).max():8.2f}")
+if len(fp):
+    for c in range(len(fp) // ncta):
+        q = fp[c * ncta:(c + 1) * ncta]
+        print(f"chunk0 call {c}: x issued {f(q[:,2]).min():8.2f}..{f(q[:,2]).max():8.2f}  f ready {f(q[:,3]).min():8.2f}..{f(q[:,3]).max():8.2f}"
+              f"  built {f(q[:,8]).min():8.2f}..{f(q[:,8]).max():8.2f}  (build med {np.median((q[:,8]-q[:,3])/1e3):.2f} us)")

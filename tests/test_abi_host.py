@@ -120,11 +120,12 @@ def test_memory_model(pb):
 def test_validation_before_launch(pb):
     # every argument error is reported before any CUDA call (no device here)
     d = pb.pb_weights(16, 8, 64, 4, 4, 0, 1.0)
-    ws = np.zeros(400000 + 256, np.uint8)
-    assert pb.pb_workspace_bytes(1, 64, 16) <= 400000
+    wsn = pb.pb_workspace_bytes(1, 64, 16)
+    assert wsn <= 4 << 20
+    ws = np.zeros(wsn + 256, np.uint8)
     wsp = (ws.ctypes.data + 255) // 256 * 256
     y = np.zeros(64, np.float32)
-    args = lambda k, a, frac=pb.PB_ACT_AUTO: (16, 1, C.byref(d), k, a, frac, y.ctypes.data, None, wsp, 400000, None)
+    args = lambda k, a, frac=pb.PB_ACT_AUTO: (16, 1, C.byref(d), k, a, frac, y.ctypes.data, None, wsp, wsn, None)
     assert pb.pb_matmul(*args(0, 16)) == pb.PB_EINVAL
     assert pb.pb_matmul(*args(5, 16)) == pb.PB_EINVAL
     assert b"k_used" in pb.pb_last_error()
@@ -140,10 +141,10 @@ def test_validation_before_launch(pb):
     assert pb.pb_matmul(16, 1, C.byref(big), 16, 32, pb.PB_ACT_AUTO, y.ctypes.data, None, wbp,
                         pb.pb_workspace_bytes(1, 1 << 17, 32), None) == pb.PB_ERANGE
     bad_off = pb.pb_weights(16, 8, 64, 4, 4, 1, 1.0)
-    assert pb.pb_matmul(16, 1, C.byref(bad_off), 1, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, 400000,
+    assert pb.pb_matmul(16, 1, C.byref(bad_off), 1, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, wsn,
                         None) == pb.PB_EINVAL
     mis = pb.pb_weights(20, 8, 64, 4, 4, 0, 1.0)   # misaligned bits
-    assert pb.pb_matmul(*(16, 1, C.byref(mis), 4, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, 400000,
+    assert pb.pb_matmul(*(16, 1, C.byref(mis), 4, 16, pb.PB_ACT_AUTO, y.ctypes.data, None, wsp, wsn,
                           None)) == pb.PB_EINVAL
     assert pb.pb_set_engine(7) == pb.PB_EINVAL
 
