@@ -313,29 +313,39 @@ def main():
     bytes_step = algo_bytes(R, K, B, k_used)
     value = bytes_step / (ms_step * 1e-3) / 1e9
 
-    # ---- per-kernel timing (same rotation, no graph): act kernel and GEMV
+    # ---- per-kernel timing (same rotation, no graph), CUDA events on the launching stream:
+    #      tensor engine: pb_matmul is ONE fused kernel (a1-a5); POPC engine: the activation
+    #      kernel + the GEMV, and the GEMV is the dominant kernel
+    fused = args.engine in ("auto", "mma") and a * B <= 32
     ev = [(torch.cuda.Event(True), torch.cuda.Event(True), torch.cuda.Event(True)) for _ in range(args.steps)]
     wsp = ws.ptr
     pstream = torch.cuda.current_stream()
-    for i in range(max(3, args.warmup)):
+
+    def one(i, timed):
         w = copies[i % M]
-        pb.check(pb.pb_act_quantize(x.data_ptr(), B, K, a, pb.PB_ACT_AUTO, wsp, ws.nbytes, pstream.cuda_stream))
-        pb.check(pb.pb_bitgemm(wsp, ws.nbytes, B, pb.C.byref(w.desc), k_used, a, y.data_ptr(), None, None, 0, 0,
-                               pstream.cuda_stream))
+        if timed:
+            ev[i][0].record()
+        if fused:
+            pb.matmul(x, w, k_used, a, y=y, ws=ws)
+        else:
+            pb.check(pb.pb_act_quantize(x.data_ptr(), B, K, a, pb.PB_ACT_AUTO, wsp, ws.nbytes, pstream.cuda_stream))
+        if timed:
+            ev[i][1].record()
+        if not fused:
+            pb.check(pb.pb_bitgemm(wsp, ws.nbytes, B, pb.C.byref(w.desc), k_used, a, y.data_ptr(), None, None, 0,
+                                   0, pstream.cuda_stream))
+        if timed:
+            ev[i][2].record()
+
+    for i in range(max(3, args.warmup)):
+        one(i, False)
     barrier()
     for i in range(args.steps):
-        w = copies[i % M]
-        ev[i][0].record()
-        pb.check(pb.pb_act_quantize(x.data_ptr(), B, K, a, pb.PB_ACT_AUTO, wsp, ws.nbytes, pstream.cuda_stream))
-        ev[i][1].record()
-        pb.check(pb.pb_bitgemm(wsp, ws.nbytes, B, pb.C.byref(w.desc), k_used, a, y.data_ptr(), None, None, 0, 0,
-                               pstream.cuda_stream))
-        ev[i][2].record()
+        one(i, True)
     barrier()
-    act_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
-    gemv_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
-    gemv_ms = max_over_ranks(gemv_ms)
-    act_ms = max_over_ranks(act_ms)
+    first_ms = max_over_ranks(statistics.mean(e[0].elapsed_time(e[1]) for e in ev))
+    second_ms = max_over_ranks(statistics.mean(e[1].elapsed_time(e[2]) for e in ev))
+    gemv_ms, act_ms = (first_ms, 0.0) if fused else (second_ms, first_ms)
     gemv_bytes = k_used * rs * K / 8          # algorithmic bytes per GEMV launch (this rank)
     achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
@@ -348,9 +358,11 @@ def main():
     except Exception:
         pass
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "bitgemm (a3-a5)", "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": gemv_bytes, "avg_launch_us": gemv_ms * 1e3,
-                "act_kernel_us": act_ms * 1e3, "gemv_share_of_step": gemv_ms / ms_step}
+                "traffic": traffic,
+                "kernel": "bitgemm_tc_kernel (fused a1-a5)" if fused else "bitgemv_popc_kernel (a3-a5)",
+                "peak_source": peak_src, "algorithmic_bytes_per_launch": gemv_bytes,
+                "avg_launch_us": gemv_ms * 1e3, "act_kernel_us": act_ms * 1e3,
+                "kernel_share_of_step": gemv_ms / ms_step}
 
     # ---- e2e through the public API with host buffers (pinned), per step:
     #      H2D x, pb matmul, D2H y.
@@ -416,14 +428,15 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": N, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": ms_step, "us_per_call": ms_step * 1e3,
                 "higher_is_better": True, "scaling": "strong" if N > 1 else "weak", "vs_baseline": None,
-                "dtype": "b1 (AND/popc) -> int32 counts -> int64 acc", "data": "synthetic",
+                "dtype": ("b1 weight/activation bits as e2m1 0/1 tensor-core products -> f32 (exact) -> int64"
+                          if fused else "b1 (AND/popc) -> int32 counts -> int64"), "data": "synthetic",
                 "config": {"workload": WORKLOAD, "R": R, "K": K, "L": L, "k_used": k_used, "act_bits": a,
                            "batch": B, "parallelism": f"rowshard{N}" if N > 1 else "single",
                            "engine": args.engine, "weight_copies": M,
                            "l2": f"inputs larger than L2: {M} rotating weight copies, "
                                  f"{M * w0.nbytes() / 2**20:.0f} MiB >= 2x L2 ({l2 / 2**20:.0f} MiB)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": (2 + (1 if (N > 1 and B > 1) else 0)) * args.steps,
+                "gpu_launches": ((1 if fused else 2) + (1 if (N > 1 and B > 1) else 0)) * args.steps,
                 "clocks": clocks, "per_L": per_L, "per_kused": per_k,
                 "context": "paper: >8x end-to-end vs FP32 on a Tesla T4 (P:28, P:216) -- context, not target"}
         print(json.dumps(line), flush=True)
