@@ -138,7 +138,7 @@ long long* debug_tl() {
     if (state == 0) {
         const char* ev = getenv("PB_TC_DEBUG");
         state = 1;
-        if (ev && atoi(ev) == 6 &&
+        if (ev && atoi(ev) >= 6 &&
             cudaMalloc(&buf, sizeof(long long) * (size_t)(10 + 10 * kTlRecords)) == cudaSuccess &&
             cudaMemset(buf, 0, sizeof(long long) * 10) == cudaSuccess)
             state = 2;

@@ -66,6 +66,15 @@ __device__ __forceinline__ double pow2d(int e) {   // 2^e, e in [-1022, 1023]
     return __hiloint2double((1023 + e) << 20, 0);
 }
 __device__ __forceinline__ long long act_cast(float v, int f, int a) {
+    if (a <= 24 && f >= -126 && f <= 127) {
+        // fp32 is exact here: v * 2^f is exact whenever |v * 2^f| >= 2^-126, smaller
+        // magnitudes truncate to 0 either way, and the clamp bounds +-2^(a-1), 2^(a-1)-1
+        // are representable for a <= 24 -- the same integer as the double form below
+        const float lim = (float)(1 << (a - 1));
+        float t = v * __int_as_float((127 + f) << 23);
+        t = fminf(fmaxf(t, -lim), lim - 1.0f);
+        return (long long)__float2int_rz(t);
+    }
     const double lim = (double)(1ll << (a - 1));
     double t = (f >= -1000 && f <= 1000) ? (double)v * pow2d(f) : ldexp((double)v, f);
     t = fmin(fmax(t, -lim), lim - 1.0);

@@ -76,6 +76,11 @@ constexpr int kActAutoFrac = -1024;           // == PB_ACT_AUTO
 #ifndef PB_MAX_WSTAGES
 #define PB_MAX_WSTAGES 16
 #endif
+#ifndef PB_TIMELINE
+#define PB_TIMELINE 0
+#endif
+constexpr bool kTimeline = PB_TIMELINE;        // per-CTA timeline / wait profiling (pb_debug_timeline)
+#define TLP(g) (kTimeline ? (g).tl : nullptr)
 constexpr int kMaxWStages = PB_MAX_WSTAGES;   // weight tile ring (stages sized per launch from free SMEM)
 constexpr uint32_t kWTileBytes = kTcRows * kChunkWords * 4;   // 16 KiB
 constexpr uint32_t kSmemMax = 227 * 1024;                       // opt-in dynamic SMEM per CTA
@@ -90,6 +95,8 @@ struct Bars {
     uint64_t q_full[kQDepth], q_empty[kQDepth];
     int2 q[kQDepth];                          // work items: units [x, y); x < 0 = no more work
     uint64_t x_ready;                        // fused path: bars.xsum written (warp 2)
+    uint64_t slice_done;                     // fused path: this CTA's slice of B written (epilogue warps)
+    uint64_t pro_done;                       // PB_TC_DEBUG=9: hold the weight prefetch until the prologue ends
     int gen;                                 // fused path: grid-barrier generation at arrival
     uint32_t tmem_base;
     int last_flag;
@@ -180,45 +187,40 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // A registers from the stored weights (pb.h), 8 32-column blocks -> 32
 // registers; register 4k + r holds in nibble e column 32k + 4e + r (the B
 // operand's order, pb_act.cu):
-//   paired storage: block k = words (P0, P1) = even / odd columns as
-//     (lower, upper) bit pairs, so nibble e of A_r is already the e2m1 code
-//     1.0*upper + 0.5*lower of column 4e + r after one mask (and a shift):
+//   KIND 0, a stored pair used whole: block k = words (P0, P1) = even / odd
+//     columns as (lower, upper) bit pairs, so nibble e of A_r is already the
+//     e2m1 code 1.0*upper + 0.5*lower of column 4e + r after one mask:
 //       A_0 = P0 & 0x33333333, A_1 = P1 & .., A_2 = (P0 >> 2) & .., A_3 = (P1 >> 2) & ..
-//     MODE 0 pair; 1 pair whose upper layer is the sign layer (complemented:
-//     P ^ 0xAAAAAAAA); 2 upper layer only (k_used odd: 0.5*upper, the pass
-//     unit becomes |S_upper|); 3 = 2 with the sign layer;
-//   canonical single layer (the last layer of an odd L): A_r = (w >> r) & 0x11111111,
-//     MODE 4; 5 = the complemented sign layer (L = 1).
-template <int MODE>
-__device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t (&v)[32]) {
+//   KIND 1, upper layer only (k_used odd): 0.5*upper (the pass unit becomes |S_upper|):
+//       A_0 = (P0 >> 1) & 0x11111111, ..., A_3 = (P1 >> 3) & 0x11111111
+//   KIND 2, canonical single layer (the last layer of an odd L): A_r = (w >> r) & 0x11111111.
+// xm complements the sign layer (pass 0): 0xAAAAAAAA (its upper bits) for KIND 0/1, ~0 for
+// KIND 2, else 0; it folds into the mask op (a 3-input LOP3) at no cost.
+template <int KIND>
+__device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t xm, uint32_t (&v)[32]) {
     const uint32_t w[16] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w,
                             q[2].x, q[2].y, q[2].z, q[2].w, q[3].x, q[3].y, q[3].z, q[3].w};
-    constexpr uint32_t kM3 = 0x33333333u, kM1 = 0x11111111u, kUp = 0xAAAAAAAAu;
+    constexpr uint32_t kM3 = 0x33333333u, kM1 = 0x11111111u;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        if (MODE <= 3) {
-            uint32_t p0 = w[2 * k], p1 = w[2 * k + 1];
-            if (MODE == 1 || MODE == 3) {
-                p0 ^= kUp;
-                p1 ^= kUp;
-            }
-            if (MODE <= 1) {
-                v[4 * k + 0] = p0 & kM3;
-                v[4 * k + 1] = p1 & kM3;
-                v[4 * k + 2] = (p0 >> 2) & kM3;
-                v[4 * k + 3] = (p1 >> 2) & kM3;
-            } else {
-                v[4 * k + 0] = (p0 >> 1) & kM1;
-                v[4 * k + 1] = (p1 >> 1) & kM1;
-                v[4 * k + 2] = (p0 >> 3) & kM1;
-                v[4 * k + 3] = (p1 >> 3) & kM1;
-            }
+        if (KIND == 0) {
+            const uint32_t p0 = w[2 * k], p1 = w[2 * k + 1];
+            v[4 * k + 0] = (p0 ^ xm) & kM3;
+            v[4 * k + 1] = (p1 ^ xm) & kM3;
+            v[4 * k + 2] = ((p0 >> 2) ^ (xm >> 2)) & kM3;
+            v[4 * k + 3] = ((p1 >> 2) ^ (xm >> 2)) & kM3;
+        } else if (KIND == 1) {
+            const uint32_t p0 = w[2 * k], p1 = w[2 * k + 1];
+            v[4 * k + 0] = ((p0 >> 1) ^ (xm >> 1)) & kM1;
+            v[4 * k + 1] = ((p1 >> 1) ^ (xm >> 1)) & kM1;
+            v[4 * k + 2] = ((p0 >> 3) ^ (xm >> 3)) & kM1;
+            v[4 * k + 3] = ((p1 >> 3) ^ (xm >> 3)) & kM1;
         } else {
-            const uint32_t c = (MODE == 5) ? ~w[k] : w[k];   // words 0..7 only
-            v[4 * k + 0] = c & kM1;
-            v[4 * k + 1] = (c >> 1) & kM1;
-            v[4 * k + 2] = (c >> 2) & kM1;
-            v[4 * k + 3] = (c >> 3) & kM1;
+            const uint32_t c = w[k];                       // words 0..7 only
+            v[4 * k + 0] = (c ^ xm) & kM1;
+            v[4 * k + 1] = ((c >> 1) ^ xm) & kM1;
+            v[4 * k + 2] = ((c >> 2) ^ xm) & kM1;
+            v[4 * k + 3] = ((c >> 3) ^ xm) & kM1;
         }
     }
 }
@@ -229,10 +231,10 @@ __device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t (&v)[32]) 
 // swizzle: chunk c of row m at c ^ (m & 7)) and the stage goes back to the TMA
 // producer before its A registers are built and stored to TMEM (32 columns
 // per 4 chunks).
-template <int MODE>
-__device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, int dbg,
-                                             uint64_t* rel0, uint64_t* rel1, int lane) {
-    constexpr bool kPair = MODE <= 3;
+template <int KIND>
+__device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
+                                             int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
+    constexpr bool kPair = KIND <= 1;
 #pragma unroll
     for (int t = 0; t < (kPair ? 2 : 1); ++t) {
         uint4 q[8];
@@ -245,10 +247,10 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
             uint32_t v[32];
             if (kPair) {
                 const uint4 qq[4] = {q[4 * h], q[4 * h + 1], q[4 * h + 2], q[4 * h + 3]};
-                build_a<MODE>(qq, v);
+                build_a<KIND>(qq, xm, v);
             } else {
                 const uint4 qq[4] = {q[2 * h], q[2 * h + 1], q[2 * h], q[2 * h + 1]};
-                build_a<MODE>(qq, v);
+                build_a<KIND>(qq, xm, v);
             }
             const int b4 = kPair ? 2 * t + h : h;
             if (dbg != 1 && dbg != 3)
@@ -262,7 +264,7 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
 // Profiling (PB_TC_DEBUG=5): accumulate cycles spent in each wait site.
 #define TWAIT(bar, ph, slotid)                                   \
     do {                                                         \
-        if (p.prof) {                                            \
+        if (kTimeline && p.prof) {                               \
             const long long _t0 = gtimer();                      \
             mbar_wait(bar, ph);                                  \
             prof[slotid] += gtimer() - _t0;                      \
@@ -333,7 +335,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 //   2. f_b (reading G8);
 //   3. the CTA's first chunk kc0 of B, built straight into B stage 0 by all 12
 //      warps, so the first MMAs wait neither for the grid barrier nor a copy;
-//   4. (converter warps) the CTA's 1/G slice of the (b, word) items of B into the
+//   4. (epilogue warps) the CTA's 1/G slice of the (b, word) items of B into the
 //      workspace tiles + its sum of x_q, published by warp 2's grid barrier.
 template <int NPAD>
 __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& p, Bars& bars, int pt,
@@ -343,7 +345,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     const int pw = pt >> 5, lane = pt & 31;
     long long tpw = 0, tmax = 0, tc0 = 0, ttr = 0;
     pdl_wait();                                        // x may be the previous kernel's output
-    if (g.tl) tpw = gtimer();
+    if TLP(g) tpw = gtimer();
     const int B = (int)g.B;
     if (pt == 0) bars.gen = ld_acquire_gpu(g.gbar + 1);
     // first-chunk items it = b * 32 + local word; warp pw takes pw, pw + 12, ...
@@ -366,8 +368,9 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         const int64_t c = 32 * (it - (int64_t)b * Wt) + lane;
         return c < g.K ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
     };
-    const float xv0 = (pw < kConvWarps && i0 + pw < i1) ? item_x(i0 + pw) : 0.f;
-    const float xv1 = (pw < kConvWarps && i0 + pw + kConvWarps < i1) ? item_x(i0 + pw + kConvWarps) : 0.f;
+    const int ew = pw - kConvWarps;                    // slice work: epilogue warps 0..3
+    const float xv0 = (ew >= 0 && i0 + ew < i1) ? item_x(i0 + ew) : 0.f;
+    const float xv1 = (ew >= 0 && i0 + ew + kEpiWarps < i1) ? item_x(i0 + ew + kEpiWarps) : 0.f;
     // ---- a1 (part 1): max|x[b,:]|
     const bool vec = (g.K & 3) == 0 && (reinterpret_cast<uintptr_t>(g.x) & 15) == 0;
     for (int b = 0; b < B; ++b) {
@@ -395,7 +398,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         if (lane == 0) bars.red[pw * kTcMaxN + b] = m;
     }
     asm volatile("bar.sync 5, 384;" ::: "memory");
-    if (g.tl) tmax = gtimer();
+    if TLP(g) tmax = gtimer();
     if (pt < B) {
         float m = bars.red[pt];
 #pragma unroll
@@ -431,17 +434,24 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         if (ia < nci) put0(ia, ma);
         if (ib < nci) put0(ib, mb);
     };
-    if (pw < nci) chunk_pair(pw, cx[0], pw + kPW, cx[1]);
-    if (pw + 2 * kPW < nci) chunk_pair(pw + 2 * kPW, cx[2], nci, 0.f);
-    for (int it = pw + 3 * kPW; it < nci; it += 2 * kPW) chunk_pair(it, chunk_x(it), it + kPW, chunk_x(it + kPW));
+#pragma unroll 1
+    for (int it = pw, k = 0; it < nci; it += 2 * kPW, k += 2) {
+        const float va = k == 0 ? cx[0] : (k == 2 ? cx[2] : chunk_x(it));
+        const float vb = k == 0 ? cx[1] : chunk_x(it + kPW);
+        chunk_pair(it, va, it + kPW, vb);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA operand reads
     asm volatile("bar.sync 5, 384;" ::: "memory");
-    if (pt == 0) mbar_arrive(&bars.b_full[0]);
-    if (g.tl) tc0 = gtimer();
-    if (pw >= kConvWarps) return;                      // the epilogue warps are done
-    // ---- the CTA's slice of the grid-wide B operand (converter warps, bar 2)
+    if (pt == 0) {
+        mbar_arrive(&bars.b_full[0]);
+        if (p.dbg == 9) mbar_arrive(&bars.pro_done);
+    }
+    if TLP(g) tc0 = gtimer();
+    if (ew < 0) return;                                // the converters go on to convert
+    // ---- the CTA's slice of the grid-wide B operand (epilogue warps, bar 1; idle until
+    // their first segment)
     int k = 0;
-    for (int64_t it = i0 + pw; it < i1; it += kConvWarps, ++k) {
+    for (int64_t it = i0 + ew; it < i1; it += kEpiWarps, ++k) {
         const int b = (int)(it / Wt);
         const int64_t w = it - (int64_t)b * Wt;
         const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
@@ -455,17 +465,18 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
         if (lane == 0) atomicAdd(&bars.xs[b], (unsigned long long)xs);
     }
-    asm volatile("bar.sync 2, 256;" ::: "memory");
-    if (pt < B) {
-        g.xsum[(int64_t)pt * kXsumStride + blockIdx.x] = (long long)bars.xs[pt];
-        if (blockIdx.x == 0) g.f[pt] = bars.f[pt];
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int et = pt - 32 * kConvWarps;
+    if (et < B) {
+        g.xsum[(int64_t)et * kXsumStride + blockIdx.x] = (long long)bars.xs[et];
+        if (blockIdx.x == 0) g.f[et] = bars.f[et];
     }
-    asm volatile("bar.sync 2, 256;" ::: "memory");
-    if (g.tl) ttr = gtimer();
-    // warp 2 (bar.sync 3) arrives at the grid barrier for this CTA once its slice is written
-    asm volatile("bar.arrive 3, 288;" ::: "memory");
-    if (g.tl && pt == 0) {
-        long long* r = tl_record(g.tl);
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if TLP(g) ttr = gtimer();
+    // warp 2 arrives at the grid barrier for this CTA once its slice is written
+    if (et == 0) mbar_arrive(&bars.slice_done);
+    if (TLP(g) && et == 0) {
+        long long* r = tl_record(TLP(g));
         if (r) {
             const long long rec[10] = {2, blockIdx.x, 0, 0, tpw, tmax, tc0, ttr, 0, 0};
             for (int q = 0; q < 10; ++q) r[q] = rec[q];
@@ -529,6 +540,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             mbar_init(&bars.q_empty[s], kQConsumers);
         }
         mbar_init(&bars.x_ready, 1);
+        mbar_init(&bars.slice_done, 1);
+        mbar_init(&bars.pro_done, 1);
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(&pmap) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&smap) : "memory");
@@ -577,6 +590,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         long long item = blockIdx.x;
         bool waited = false;
         int tc = 0;
+        if (p.dbg == 9 && g.x) mbar_wait(&bars.pro_done, 0);
         while (true) {
             mbar_wait(&bars.q_empty[qi], qph ^ 1);
             const long long u0 = item < p.items ? item * p.Gu : -1;
@@ -638,7 +652,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         bool published = false;
         auto wait_published = [&]() {
             if (g.x && !published) {
-                asm volatile("bar.sync 3, 288;" ::: "memory");         // this CTA's slice is written
+                mbar_wait(&bars.slice_done, 0);                        // this CTA's slice is written
                 if (lane == 0) {
                     // generation-based grid barrier; the arrival count is left zero.  The
                     // CTA's writes are ordered before the arrival by bar.sync + this
@@ -654,7 +668,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 __syncwarp();
                 while (ld_acquire_gpu(g.gbar + 1) == bars.gen) __nanosleep(32);   // every CTA has arrived
                 asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> bulk-copy reads
-                if (g.tl && lane == 0) bars.t_b = gtimer();
+                if (TLP(g) && lane == 0) bars.t_b = gtimer();
                 // sum_c x_q[b, c] from every CTA's partial, for the epilogue
                 for (int b = 0; b < (int)g.B; ++b) {
                     unsigned long long t = 0;
@@ -669,7 +683,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 published = true;
             }
         };
-        if (!g.x && g.tl && lane == 0) bars.t_b = gtimer();
+        if (!g.x && TLP(g) && lane == 0) bars.t_b = gtimer();
         int cc = 0;
         while (true) {
             const int2 it = take_item(bars, qi, qph, lane);
@@ -724,7 +738,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         const bool open = first && u == us;
                         TWAIT(&bars.a_full[slot], phase, 2);
                         tc_fence_after();
-                        if (g.tl && t_mma0 == 0) t_mma0 = gtimer();
+                        if (TLP(g) && t_mma0 == 0) t_mma0 = gtimer();
                         if (p.dbg == 2 || p.dbg == 3) {
                             if (elect_one()) tc_commit(&bars.a_empty[slot]);
                         } else if (elect_one()) {
@@ -749,7 +763,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 __syncwarp();
             }
         }
-        if (g.tl && lane == 0) {
+        if (TLP(g) && lane == 0) {
             bars.t_mma0 = t_mma0;
             bars.t_mend = gtimer();
         }
@@ -779,7 +793,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.a_full[pend_slot]);
                 pend_slot = -1;
-                if (g.tl && warp == kConv0 && lane == 0 && npub++ == 0) bars.t_cv[3] = gtimer();
+                if (TLP(g) && warp == kConv0 && lane == 0 && npub++ == 0) bars.t_cv[3] = gtimer();
             }
         };
         while (true) {
@@ -795,28 +809,27 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         continue;
                     }
                     const int st0 = tc % p.wstages, st1 = (tc + ntile - 1) % p.wstages;
-                    if (g.tl && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[0] = gtimer();
+                    if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[0] = gtimer();
                     TWAIT(&bars.w_full[st0], (uint32_t)((tc / p.wstages) & 1), 3);
                     if (stored_pair) TWAIT(&bars.w_full[st1], (uint32_t)(((tc + 1) / p.wstages) & 1), 3);
-                    if (g.tl && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[1] = gtimer();
+                    if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[1] = gtimer();
                     publish();                          // previous pass's A is in TMEM: tell the MMA
                     TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
                     tc_fence_after();
-                    const int mode = stored_pair ? (use_lo ? 0 : 2) + (ps == 0 ? 1 : 0) : (ps == 0 ? 5 : 4);
+                    const int kind = stored_pair ? (use_lo ? 0 : 1) : 2;
+                    const uint32_t xm = ps == 0 ? (stored_pair ? 0xAAAAAAAAu : 0xFFFFFFFFu) : 0u;
                     const uint32_t t0 = wtile_s + (uint32_t)st0 * kWTileBytes;
                     const uint32_t t1 = wtile_s + (uint32_t)st1 * kWTileBytes;
                     const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
                     uint64_t* r0 = &bars.w_empty[st0];
                     uint64_t* r1 = &bars.w_empty[st1];
-                    switch (mode) {
-                        case 0: convert_pass<0>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
-                        case 1: convert_pass<1>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
-                        case 2: convert_pass<2>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
-                        case 3: convert_pass<3>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
-                        case 4: convert_pass<4>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
-                        default: convert_pass<5>(t0, t1, swz, dst, p.dbg, r0, r1, lane); break;
-                    }
-                    if (g.tl && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
+                    if (kind == 0)
+                        convert_pass<0>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
+                    else if (kind == 1)
+                        convert_pass<1>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
+                    else
+                        convert_pass<2>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
+                    if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
                     tc += ntile;
                     pend_slot = slot;
                     slot += 2;
@@ -881,7 +894,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 mbar_wait(&bars.d_full[db], (uint32_t)((seg >> 1) & 1));
                 tc_fence_after();
                 long long te[3] = {0, 0, 0};
-                if (g.tl) te[0] = gtimer();
+                if TLP(g) te[0] = gtimer();
                 // tot_b = sum_j T_j sum_r |S_lo(r)| D_r[b*a + j]; lo(r) = least significant layer of group r
                 for (int r = 0; r < p.regions; ++r) {
                     int last = (r + 1) * p.Gp - 1;
@@ -909,14 +922,14 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.d_empty[db]);
-                if (g.tl) te[1] = gtimer();
+                if TLP(g) te[1] = gtimer();
                 // exact integer adds into the tile's accumulator (order-independent); no
                 // round trip here: tiles are finalised after the end-of-work grid barrier
                 unsigned long long* ab = g.accbuf + (int64_t)rt * g.B * kTcRows + m;
                 for (int b = 0; b < g.B; ++b) red_add_u64(ab + b * kTcRows, s_tot[b * kTcRows + m]);
-                if (g.tl && ew == 0 && lane == 0) {
+                if (TLP(g) && ew == 0 && lane == 0) {
                     te[2] = gtimer();
-                    long long* rr = tl_record(g.tl);
+                    long long* rr = tl_record(TLP(g));
                     if (rr) {
                         const long long rec[10] = {3, blockIdx.x, seg, kcB - kcA, te[0], te[1], te[2], te[2], 0, 0};
                         for (int k = 0; k < 10; ++k) rr[k] = rec[k];
@@ -952,12 +965,12 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 if (row < g.R) finish(b, row, t);
             }
         }
-        if (g.tl && ew == 0 && lane == 0) bars.t_cend = gtimer();
+        if (TLP(g) && ew == 0 && lane == 0) bars.t_cend = gtimer();
     }
 
-    if (p.prof && g.tl && lane == 0) {
+    if (kTimeline && p.prof && TLP(g) && lane == 0) {
         // wait totals (ns): w_empty, b_full, a_full, w_full, a_empty
-        long long* r = tl_record(g.tl);
+        long long* r = tl_record(TLP(g));
         if (r) {
             const long long rec[10] = {4, blockIdx.x, warp, gtimer() - g_start, prof[0], prof[1], prof[2], prof[3],
                                        prof[4], 0};
@@ -966,8 +979,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     }
     tc_fence_before();
     __syncthreads();
-    if (g.tl && warp == 1 && lane == 0) {
-        long long* r = tl_record(g.tl);
+    if (TLP(g) && warp == 1 && lane == 0) {
+        long long* r = tl_record(TLP(g));
         if (r) {
             unsigned smid;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -975,7 +988,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                                        bars.t_cend, gtimer()};
             for (int k = 0; k < 10; ++k) r[k] = rec[k];
         }
-        long long* r5 = tl_record(g.tl);
+        long long* r5 = tl_record(TLP(g));
         if (r5) {
             const long long rec[10] = {5, blockIdx.x, bars.t_c0s[0], bars.t_c0s[1], bars.t_cv[0], bars.t_cv[1],
                                        bars.t_cv[2], bars.t_cv[3], bars.t_c0, 0};
