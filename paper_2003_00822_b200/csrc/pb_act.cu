@@ -103,8 +103,8 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
         if (npad) {
             // lane j < a writes plane row n = b*a + j; the last batch column zeroes rows [a*B, npad)
             if (lane < a) put_b_operand(bexp, npad, w, b * a + lane, mine);
-            if (b == (int)gridDim.y - 1 && (int)gridDim.y * a + lane < npad)
-                put_b_operand(bexp, npad, w, (int)gridDim.y * a + lane, 0u);
+            if (b == (int)gridDim.y - 1)
+                for (int n = (int)gridDim.y * a + lane; n < npad; n += 32) put_b_operand(bexp, npad, w, n, 0u);
         }
     }
 #pragma unroll
@@ -175,7 +175,8 @@ cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kword
                               reinterpret_cast<int32_t*>(base + l.off_f),
                               reinterpret_cast<long long*>(base + l.off_xsum),
                               reinterpret_cast<uint32_t*>(base + l.off_planes),
-                              reinterpret_cast<uint8_t*>(base + l.off_bexp), l.npad, debug_tl());
+                              reinterpret_cast<uint8_t*>(base + l.off_bexp),
+                              tc_npad(B, a) == l.npad ? l.npad : 0, debug_tl());
 }
 
 }  // namespace pb

@@ -462,7 +462,7 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     g.bias = bias;
     g.fn = fn;
     g.accumulate = accumulate ? 1 : 0;
-    g.npad = l.npad;
+    g.npad = pb::tc_npad(batch, act_bits);     // whole batch in one tensor-engine launch (else 0)
     g.bexp = reinterpret_cast<uint8_t*>(base + l.off_bexp);
     g.accbuf = reinterpret_cast<unsigned long long*>(base + l.off_slots);
     g.counters = reinterpret_cast<int*>(base + l.off_count);
@@ -477,16 +477,34 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     cudaError_t e;
     const cudaStream_t cs = static_cast<cudaStream_t>(s);
     if (x) {
-        if (g_engine == PB_ENGINE_POPC || !pb::tc_supported(g)) return PB_EINVAL;
-        g.x = x;
-        e = pb::launch_gemm_tc(g, cs);
-        if (e != cudaSuccess) return cuda_fail(e, "fused bitgemm launch");
+        // fused a1-a5, one launch per batch slice of <= 64 plane columns (pb::tc_slice); every
+        // slice must fit the tensor engine, else the caller runs the split path
+        if (g_engine == PB_ENGINE_POPC) return PB_EINVAL;
+        const int64_t bs = pb::tc_slice(batch, act_bits);
+        pb::GemmArgs gs = g;
+        for (int64_t b0 = 0; b0 < batch; b0 += bs) {
+            gs.B = batch - b0 < bs ? batch - b0 : bs;
+            gs.npad = pb::tc_npad(gs.B, act_bits);
+            if (!pb::tc_supported(gs)) return PB_EINVAL;
+        }
+        for (int64_t b0 = 0; b0 < batch; b0 += bs) {
+            gs.B = batch - b0 < bs ? batch - b0 : bs;
+            gs.npad = pb::tc_npad(gs.B, act_bits);
+            gs.x = x + b0 * w->cols;
+            gs.y = y + b0 * w->rows;
+            gs.acc = acc ? reinterpret_cast<long long*>(acc) + b0 * w->rows : nullptr;
+            gs.f = g.f + b0;
+            gs.xsum = g.xsum + b0 * pb::kXsumStride;
+            e = pb::launch_gemm_tc(gs, cs);
+            if (e != cudaSuccess) return cuda_fail(e, "fused bitgemm launch");
+        }
         *fused_done = true;
         return PB_OK;
     }
     if (g_engine == PB_ENGINE_MMA) {
         if (!pb::tc_supported(g))
-            return fail(PB_EINVAL, "PB_ENGINE_MMA needs act_bits*batch <= 32 and k_used*N_pad <= 256");
+            return fail(PB_EINVAL, "PB_ENGINE_MMA on the split path needs act_bits*batch <= 64, batch <= 32 "
+                                   "and rows <= 262144");
         e = pb::launch_gemm_tc(g, cs);
     } else if (g_engine == PB_ENGINE_AUTO && pb::tc_supported(g)) {
         e = pb::launch_gemm_tc(g, cs);

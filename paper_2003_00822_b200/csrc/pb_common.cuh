@@ -65,6 +65,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ double pow2d(int e) {   // 2^e, e in [-1022, 1023]
     return __hiloint2double((1023 + e) << 20, 0);
 }
+static __device__ __noinline__ long long act_cast_f64(float v, int f, int a) {
+    const double lim = (double)(1ll << (a - 1));
+    double t = (f >= -1000 && f <= 1000) ? (double)v * pow2d(f) : ldexp((double)v, f);
+    t = fmin(fmax(t, -lim), lim - 1.0);
+    return __double2ll_rz(t);
+}
 __device__ __forceinline__ long long act_cast(float v, int f, int a) {
     if (a <= 24 && f >= -126 && f <= 127) {
         // fp32 is exact here: v * 2^f is exact whenever |v * 2^f| >= 2^-126, smaller
@@ -75,10 +81,7 @@ __device__ __forceinline__ long long act_cast(float v, int f, int a) {
         t = fminf(fmaxf(t, -lim), lim - 1.0f);
         return (long long)__float2int_rz(t);
     }
-    const double lim = (double)(1ll << (a - 1));
-    double t = (f >= -1000 && f <= 1000) ? (double)v * pow2d(f) : ldexp((double)v, f);
-    t = fmin(fmax(t, -lim), lim - 1.0);
-    return __double2ll_rz(t);
+    return act_cast_f64(v, f, a);                       // a > 24 or an extreme literal act_frac
 }
 // f_b from max|x[b,:]| (reading G8): the largest f with max|x| * 2^f < 2^(a-1).
 __device__ __forceinline__ int act_frac_of(float m, int a) {

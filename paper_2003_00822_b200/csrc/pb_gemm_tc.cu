@@ -104,10 +104,10 @@ struct Bars {
     long long t_c0, t_cv[4];                 // first chunk built; converter warp 3's first pass
     long long t_c0s[2];                      // first chunk: x loads issued, f_b available
     // fused activation prologue
-    float red[12 * kTcMaxN];                 // per-warp partial max|x[b,:]| (prologue warps)
-    int f[kTcMaxN];                          // f_b
-    unsigned long long xs[kTcMaxN];          // this CTA's sum of x_q[b, slice]
-    unsigned long long xsum[kTcMaxN];        // sum_c x_q[b, c] over all CTAs
+    float red[12 * kTcMaxB];                 // per-warp partial max|x[b,:]| (prologue warps)
+    int f[kTcMaxB];                          // f_b
+    unsigned long long xs[kTcMaxB];          // this CTA's sum of x_q[b, slice]
+    unsigned long long xsum[kTcMaxB];        // sum_c x_q[b, c] over all CTAs
 };
 static_assert(sizeof(Bars) <= kHdrBytes, "Bars must fit the SMEM header");
 
@@ -360,13 +360,15 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     for (int k = 0; k < 3; ++k) cx[k] = chunk_x(pw + kPW * k);
     // slice items (converter warps): words up to the last chunk's end (zero B for the K
     // tail, where the complemented sign layer is 1)
-    const int64_t Wt = (int64_t)p.chunks * kChunkWords, N = (int64_t)B * Wt;
-    const int64_t G = gridDim.x;
-    const int64_t i0 = N * blockIdx.x / G, i1 = N * (blockIdx.x + 1) / G;
-    auto item_x = [&](int64_t it) -> float {
-        const int b = (int)(it / Wt);
-        const int64_t c = 32 * (it - (int64_t)b * Wt) + lane;
-        return c < g.K ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
+    // (32-bit index math: N = B * Wt < 2^31 is checked by make_plan)
+    const uint32_t Wt = (uint32_t)p.chunks * kChunkWords, N = (uint32_t)B * Wt;
+    const uint32_t G = gridDim.x;
+    const uint32_t nq = N / G, nr = N - nq * G;        // floor(N * c / G) without 64-bit division
+    const uint32_t i0 = nq * blockIdx.x + nr * blockIdx.x / G, i1 = nq * (blockIdx.x + 1) + nr * (blockIdx.x + 1) / G;
+    auto item_x = [&](uint32_t it) -> float {
+        const uint32_t b = it / Wt;
+        const uint32_t c = 32 * (it - b * Wt) + lane;
+        return c < (uint32_t)g.K ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
     };
     const int ew = pw - kConvWarps;                    // slice work: epilogue warps 0..3
     const float xv0 = (ew >= 0 && i0 + ew < i1) ? item_x(i0 + ew) : 0.f;
@@ -391,18 +393,19 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
                     m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
             }
         } else {
+#pragma unroll 1
             for (int64_t c = pt; c < g.K; c += kPT) m = fmaxf(m, fabsf(__ldg(xb + c)));
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) bars.red[pw * kTcMaxN + b] = m;
+        if (lane == 0) bars.red[pw * kTcMaxB + b] = m;
     }
     asm volatile("bar.sync 5, 384;" ::: "memory");
     if TLP(g) tmax = gtimer();
     if (pt < B) {
         float m = bars.red[pt];
 #pragma unroll
-        for (int w = 1; w < kPW; ++w) m = fmaxf(m, bars.red[w * kTcMaxN + pt]);
+        for (int w = 1; w < kPW; ++w) m = fmaxf(m, bars.red[w * kTcMaxB + pt]);
         bars.f[pt] = (g.act_frac == kActAutoFrac) ? act_frac_of(m, g.a) : g.act_frac;
         bars.xs[pt] = 0;
     }
@@ -425,7 +428,8 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     auto put0 = [&](int it, uint32_t mine) {
         const int b = it / kChunkWords, wl = it - b * kChunkWords;
         if (lane < g.a) put_b_operand(bstage0, NPAD, wl, b * g.a + lane, mine);
-        if (b == B - 1 && B * g.a + lane < NPAD) put_b_operand(bstage0, NPAD, wl, B * g.a + lane, 0u);
+        if (b == B - 1)
+            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand(bstage0, NPAD, wl, n, 0u);
     };
     auto chunk_pair = [&](int ia, float va, int ib, float vb) {
         uint32_t ma, mb;
@@ -451,15 +455,17 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     // ---- the CTA's slice of the grid-wide B operand (epilogue warps, bar 1; idle until
     // their first segment)
     int k = 0;
-    for (int64_t it = i0 + ew; it < i1; it += kEpiWarps, ++k) {
-        const int b = (int)(it / Wt);
-        const int64_t w = it - (int64_t)b * Wt;
+#pragma unroll 1
+    for (uint32_t it = i0 + ew; it < i1; it += kEpiWarps, ++k) {
+        const uint32_t b = it / Wt;
+        const uint32_t w = it - b * Wt;
         const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
         const long long q = act_cast(v, bars.f[b], g.a);
         uint32_t mine, dummy;
         transpose2(q, 0, mine, dummy);
         if (lane < g.a) put_b_operand(g.bexp, NPAD, w, b * g.a + lane, mine);
-        if (b == B - 1 && B * g.a + lane < NPAD) put_b_operand(g.bexp, NPAD, w, B * g.a + lane, 0u);
+        if (b == B - 1)
+            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand(g.bexp, NPAD, w, n, 0u);
         long long xs = q;
 #pragma unroll
         for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
@@ -670,10 +676,12 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> bulk-copy reads
                 if (TLP(g) && lane == 0) bars.t_b = gtimer();
                 // sum_c x_q[b, c] from every CTA's partial, for the epilogue
+#pragma unroll 1
                 for (int b = 0; b < (int)g.B; ++b) {
                     unsigned long long t = 0;
-                    for (int c = lane; c < (int)G; c += 32)
-                        t += (unsigned long long)__ldcg(g.xsum + (int64_t)b * kXsumStride + c);
+                    const long long* xs = g.xsum + b * kXsumStride;
+#pragma unroll 1
+                    for (int c = lane; c < (int)G; c += 32) t += (unsigned long long)__ldcg(xs + c);
 #pragma unroll
                     for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
                     if (lane == 0) bars.xsum[b] = t;
@@ -852,7 +860,6 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0);
         bool have_xsum = false;
-        unsigned long long sxs[kTcMaxN / 8];   // sum_c x_q[b, c] for b < B (B <= 32 / a <= 4 with a >= 8)
         auto xsum_of = [&](int b) -> unsigned long long {
             if (g.x) {
                 if (!have_xsum) {
@@ -862,10 +869,11 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 return bars.xsum[b];
             }
             unsigned long long sx = 0;
-            for (int pp = 0; pp < g.nsplit; ++pp) sx += (unsigned long long)g.xsum[(int64_t)b * kXsumStride + pp];
+            const long long* xs = g.xsum + b * kXsumStride;
+#pragma unroll 1
+            for (int pp = 0; pp < g.nsplit; ++pp) sx += (unsigned long long)xs[pp];
             return sx;
         };
-        (void)sxs;
         auto finish = [&](int b, int64_t row, unsigned long long t) {
             t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
             const long long accv = (long long)t;
@@ -900,21 +908,25 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     int last = (r + 1) * p.Gp - 1;
                     if (last > p.passes - 1) last = p.passes - 1;
                     const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
-                    uint32_t dv[NPAD];
-                    ld_tmem_cols<NPAD>(tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD), dv);
-                    tmem_ld_wait();
                     unsigned long long acc = 0;
                     int j = 0, bc = 0;
+#pragma unroll 1
+                    for (int c8 = 0; c8 < NPAD && bc < g.B; c8 += 8) {
+                        uint32_t dv[8];
+                        ld_tmem_x8(tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD + c8), dv);
+                        tmem_ld_wait();
 #pragma unroll
-                    for (int n = 0; n < NPAD; ++n) {
-                        if (bc < g.B) {
-                            acc += plane_scale(g.a, j) * (wr * (unsigned long long)__float2uint_rn(__uint_as_float(dv[n])));
-                            if (++j == g.a) {
-                                if (r == 0) s_tot[bc * kTcRows + m] = acc;
-                                else s_tot[bc * kTcRows + m] += acc;
-                                acc = 0;
-                                j = 0;
-                                ++bc;
+                        for (int e = 0; e < 8; ++e) {
+                            if (bc < g.B) {
+                                acc += plane_scale(g.a, j) *
+                                       (wr * (unsigned long long)__float2uint_rn(__uint_as_float(dv[e])));
+                                if (++j == g.a) {
+                                    if (r == 0) s_tot[bc * kTcRows + m] = acc;
+                                    else s_tot[bc * kTcRows + m] += acc;
+                                    acc = 0;
+                                    j = 0;
+                                    ++bc;
+                                }
                             }
                         }
                     }
@@ -1045,7 +1057,7 @@ int ceil_log2_i(int64_t v) {
 // The plan for a shape, or false when the tensor engine does not cover it.
 bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
 {
-    if (npad <= 0 || g.kwords <= 0 || g.R <= 0 || g.B <= 0 || g.L > 16) return false;
+    if (npad <= 0 || g.kwords <= 0 || g.R <= 0 || g.B <= 0 || g.B > kTcMaxB || g.L > 16) return false;
     p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
     if (p.tiles > kAccTiles) return false;
     p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
@@ -1064,6 +1076,7 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     if (p.slots > kMaxSlots) p.slots = kMaxSlots;
     if (p.slots < 2) return false;
     // work items of >= ~4 passes (so an item's epilogue keeps up with its MMAs)
+    if ((long long)g.B * p.chunks * kChunkWords >= (1ll << 31)) return false;   // prologue index math
     p.Gu = (4 + p.passes - 1) / p.passes;
     p.items = (p.units + p.Gu - 1) / p.Gu;
     return true;
@@ -1135,6 +1148,7 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, cudaStream_t s)
         case 8: return launch_t<8>(g, s);
         case 16: return launch_t<16>(g, s);
         case 32: return launch_t<32>(g, s);
+        case 64: return launch_t<64>(g, s);
         default: return cudaErrorNotSupported;
     }
 }

@@ -11,7 +11,8 @@ namespace pb {
 constexpr int kMaxSplit = 64;        // activation kernel CTAs per batch column (max)
 constexpr size_t kAlign = 256;
 constexpr int kTcRows = 128;         // tensor engine row tile (MMA M)
-constexpr int kTcMaxN = 32;          // tensor engine: a * batch <= 32 (MMA N padded to 8/16/32)
+constexpr int kTcMaxN = 64;          // tensor engine: a * batch <= 64 per launch (MMA N padded to 8/16/32/64)
+constexpr int kTcMaxB = 32;          // tensor engine: batch columns per launch
 
 inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
 
@@ -19,8 +20,16 @@ inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a
 // 0 when the tensor engine's operand tiles are not produced for this shape.
 inline int tc_npad(int64_t batch, int32_t a) {
     const int64_t n = batch * a;
-    if (n <= 0 || n > kTcMaxN) return 0;
-    return n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+    if (n <= 0 || n > kTcMaxN || batch > kTcMaxB) return 0;
+    return n <= 8 ? 8 : (n <= 16 ? 16 : (n <= 32 ? 32 : 64));
+}
+// Batch columns per tensor-engine launch: the whole batch when it fits, else slices of
+// min(32, 64 / a) columns (pb_matmul / pb_linear run one fused launch per slice).
+inline int64_t tc_slice(int64_t batch, int32_t a) {
+    if (tc_npad(batch, a) > 0 || a <= 0) return batch;
+    int64_t s = kTcMaxN / a;
+    if (s > kTcMaxB) s = kTcMaxB;
+    return s < 1 ? 1 : s;
 }
 
 // Workspace carve-up (documented in pb.h, pb_workspace_bytes):
@@ -49,10 +58,11 @@ struct WsLayout {
 };
 inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     WsLayout l;
-    l.npad = tc_npad(batch, act_bits);
+    const int64_t bs = tc_slice(batch, act_bits);          // tensor-engine operands per slice
+    l.npad = tc_npad(bs, act_bits);
     l.off_count = 0;
     l.off_slots = align_up(sizeof(int32_t) * (kMaxTiles + 6));
-    const size_t slots = l.npad ? sizeof(long long) * kAccTiles * (size_t)batch * kTcRows : 0;
+    const size_t slots = l.npad ? sizeof(long long) * kAccTiles * (size_t)bs * kTcRows : 0;
     l.off_f = align_up(l.off_slots + slots);
     l.off_xsum = align_up(l.off_f + sizeof(int32_t) * (size_t)batch);
     l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kXsumStride);

@@ -68,6 +68,10 @@ CASES = [  # R, K, B, L, k_used, a
     (65, 4109, 1, 12, 6, 31),
     (130, 129, 5, 16, 9, 3),
     (512, 2048, 16, 6, 6, 16),
+    (300, 2000, 4, 8, 8, 16),     # N = 64 in one tensor-engine launch
+    (257, 1030, 3, 5, 4, 16),     # N = 48 -> padded to 64
+    (129, 3000, 8, 8, 7, 8),      # N = 64, a = 8
+    (200, 1500, 37, 4, 4, 16),    # 10 slices of <= 4 columns, ragged last slice
 ]
 
 
