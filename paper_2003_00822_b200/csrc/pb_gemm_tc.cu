@@ -72,6 +72,7 @@ constexpr int kQDepth = 16;                   // work-item queue (warp 0 -> ever
 constexpr int kMaxSlots = 4;                  // A ring: up to 4 slots x 128 TMEM columns (16 MMAs each)
 constexpr int kMaxRegions = 4;                // TMEM accumulators: sign layer + magnitude groups
 constexpr int kChunkWords = 32;               // K-chunk = one 128-byte swizzle row
+constexpr int kMaxBStages = 4;                // B (plane tile) ring: 2, or 4 when a unit is short
 constexpr int kActAutoFrac = -1024;           // == PB_ACT_AUTO
 #ifndef PB_MAX_WSTAGES
 #define PB_MAX_WSTAGES 16
@@ -90,17 +91,18 @@ constexpr uint32_t kHdrBytes = 4096;                          // struct Bars
 struct Bars {
     uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];   // a_full: the 4 warps of one h-set
     uint64_t w_full[kMaxWStages], w_empty[kMaxWStages];
-    uint64_t b_full[2], b_empty[2];
+    uint64_t b_full[kMaxBStages], b_empty[kMaxBStages];
     uint64_t d_full[2], d_empty[2];           // double-buffered accumulators (segment parity)
     uint64_t q_full[kQDepth], q_empty[kQDepth];
     int2 q[kQDepth];                          // work items: units [x, y); x < 0 = no more work
     uint64_t x_ready;                        // fused path: bars.xsum written (warp 2)
     uint64_t slice_done;                     // fused path: this CTA's slice of B written (epilogue warps)
-    uint64_t pro_done;                       // PB_TC_DEBUG=9: hold the weight prefetch until the prologue ends
-    int gen;                                 // fused path: grid-barrier generation at arrival
+    uint64_t pro_done;                       // fused path: first chunk's B built (converters resume)
+    unsigned long long gbase;                // fused path: prologue grid-barrier counter base (grid_base)
     uint32_t tmem_base;
     int last_flag;
     long long t_b, t_mma0, t_mend, t_cend;   // diagnostics timeline (globaltimer ns)
+    long long t_eseg[3], t_ebar[2];          // tail: last segment wake/drained/added; end barrier arrive/exit
     long long t_c0, t_cv[4];                 // first chunk built; converter warp 3's first pass
     long long t_c0s[2];                      // first chunk: x loads issued, f_b available
     // fused activation prologue
@@ -283,6 +285,8 @@ struct TcPlan {
     long long units;  // tiles * chunks
     int slots, sf_col, d_col;
     int wstages;      // weight tile ring depth
+    int bstages;      // B (plane tile) ring depth: a B copy is an L2 round trip, hidden only
+                      // when the stages cover it (units of 1-2 passes take ~0.5-1 us of MMAs)
     int passes;       // ceil(k_used / 2): layer pairs (0,1), (2,3), ...
     int Gp;           // passes per accumulator group (<= G/2 layers pairs, K * 2^G <= 2^24)
     int regions;      // ceil(passes / Gp)
@@ -321,45 +325,80 @@ __device__ __forceinline__ unsigned long long layer_mag(int L, int offset, int i
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void st_shared_u64(uint32_t a, unsigned long long v) {
+    asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_shared_u64(uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return v;
+}
+// Grid barriers on monotonic 64-bit counters in the workspace: every barrier
+// instance adds exactly kGridStride in total (CTA 0 adds kGridStride - (G-1), the
+// others 1) with one fire-and-forget red.release each, so nothing is reset and no
+// arrival waits for a returned value.  A CTA reads the counter after its PDL wait
+// (every earlier call has completed, and no instance of this call can complete
+// before this CTA arrives): the instance's base is that value rounded down to a
+// multiple of kGridStride, and it is complete once the counter reaches base + stride.
+constexpr unsigned long long kGridStride = 1ull << 20;
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long grid_base(const int* ctr) {
+    return ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(ctr)) & ~(kGridStride - 1);
+}
+__device__ __forceinline__ void grid_arrive(int* ctr) {
+    const unsigned long long v = blockIdx.x == 0 ? kGridStride - (gridDim.x - 1) : 1ull;
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void grid_wait(const int* ctr, unsigned long long base) {
+    const unsigned long long* c = reinterpret_cast<const unsigned long long*>(ctr);
+    while (ld_acquire_gpu_u64(c) < base + kGridStride) {
+    }
+}
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 // Fused steps a1-a2 (same arithmetic as pb_act.cu), run at
-// kernel start by the 384 converter + epilogue threads (warps 3..14, bar 5)
-// while warp 0 already streams weight tiles:
+// kernel start by the 4 epilogue warps (128 threads, bar 5; idle until their first
+// segment) while warp 0 streams weight tiles and the converters already build A
+// from them (A does not depend on x):
 //   1. one load wave: max|x[b,:]| over all of x (every CTA re-reads the
 //      L2-resident B*K floats), plus the values of the CTA's first chunk and of
 //      its slice of the grid-wide B operand;
 //   2. f_b (reading G8);
-//   3. the CTA's first chunk kc0 of B, built straight into B stage 0 by all 12
-//      warps, so the first MMAs wait neither for the grid barrier nor a copy;
-//   4. (epilogue warps) the CTA's 1/G slice of the (b, word) items of B into the
-//      workspace tiles + its sum of x_q, published by warp 2's grid barrier.
+//   3. the CTA's first chunk kc0 of B, built straight into B stage 0, so the
+//      first MMAs wait neither for the grid barrier nor a copy;
+//   4. the CTA's 1/G slice of the (b, word) items of B into the workspace tiles
+//      + its sum of x_q, published by warp 2's grid barrier.
 template <int NPAD>
 __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& p, Bars& bars, int pt,
                                                uint8_t* bstage0, int kc0) {
-    constexpr int kPW = kConvWarps + kEpiWarps;        // 12 warps
+    constexpr int kPW = kEpiWarps;                     // 4 warps
     constexpr int kPT = 32 * kPW;
+    constexpr int kCx = 8;                             // first-chunk values prefetched per thread
     const int pw = pt >> 5, lane = pt & 31;
-    long long tpw = 0, tmax = 0, tc0 = 0, ttr = 0;
+    long long tpw = 0, tmax = 0, tc0 = 0, ttr = 0, tfb = 0, tcg = 0;
     pdl_wait();                                        // x may be the previous kernel's output
     if TLP(g) tpw = gtimer();
     const int B = (int)g.B;
-    if (pt == 0) bars.gen = ld_acquire_gpu(g.gbar + 1);
-    // first-chunk items it = b * 32 + local word; warp pw takes pw, pw + 12, ...
+    if (pt == 0) bars.gbase = grid_base(g.gbar);
+    // first-chunk items it = b * 32 + local word; warp pw takes pw, pw + 4, ...
     const int nci = B * kChunkWords;
     auto chunk_x = [&](int it) -> float {
         const int b = it / kChunkWords;
         const int64_t c = 32 * ((int64_t)kc0 * kChunkWords + (it - b * kChunkWords)) + lane;
         return (it < nci && c < g.K) ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
     };
-    float cx[3];
+    float cx[kCx];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) cx[k] = chunk_x(pw + kPW * k);
-    // slice items (converter warps): words up to the last chunk's end (zero B for the K
-    // tail, where the complemented sign layer is 1)
+    for (int k = 0; k < kCx; ++k) cx[k] = chunk_x(pw + kPW * k);
+    // slice items: words up to the last chunk's end (zero B for the K tail, where the
+    // complemented sign layer is 1)
     // (32-bit index math: N = B * Wt < 2^31 is checked by make_plan)
     const uint32_t Wt = (uint32_t)p.chunks * kChunkWords, N = (uint32_t)B * Wt;
     const uint32_t G = gridDim.x;
@@ -370,9 +409,9 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         const uint32_t c = 32 * (it - b * Wt) + lane;
         return c < (uint32_t)g.K ? __ldg(g.x + (int64_t)b * g.K + c) : 0.f;
     };
-    const int ew = pw - kConvWarps;                    // slice work: epilogue warps 0..3
-    const float xv0 = (ew >= 0 && i0 + ew < i1) ? item_x(i0 + ew) : 0.f;
-    const float xv1 = (ew >= 0 && i0 + ew + kEpiWarps < i1) ? item_x(i0 + ew + kEpiWarps) : 0.f;
+    const int ew = pw;
+    const float xv0 = (i0 + ew < i1) ? item_x(i0 + ew) : 0.f;
+    const float xv1 = (i0 + ew + kEpiWarps < i1) ? item_x(i0 + ew + kEpiWarps) : 0.f;
     // ---- a1 (part 1): max|x[b,:]|
     const bool vec = (g.K & 3) == 0 && (reinterpret_cast<uintptr_t>(g.x) & 15) == 0;
     for (int b = 0; b < B; ++b) {
@@ -381,15 +420,15 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         if (vec) {
             const float4* x4 = reinterpret_cast<const float4*>(xb);
             const int64_t n4 = g.K / 4;
-            for (int64_t c0 = pt; c0 < n4; c0 += 12 * kPT) {    // 12 loads in flight per thread
-                float4 v[12];
+            for (int64_t c0 = pt; c0 < n4; c0 += 16 * kPT) {    // 16 loads in flight per thread
+                float4 v[16];
 #pragma unroll
-                for (int u = 0; u < 12; ++u) {
+                for (int u = 0; u < 16; ++u) {
                     const int64_t c = c0 + (int64_t)u * kPT;
                     v[u] = c < n4 ? __ldg(x4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
-                for (int u = 0; u < 12; ++u)
+                for (int u = 0; u < 16; ++u)
                     m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
             }
         } else {
@@ -400,7 +439,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0) bars.red[pw * kTcMaxB + b] = m;
     }
-    asm volatile("bar.sync 5, 384;" ::: "memory");
+    asm volatile("bar.sync 5, 128;" ::: "memory");
     if TLP(g) tmax = gtimer();
     if (pt < B) {
         float m = bars.red[pt];
@@ -409,7 +448,8 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         bars.f[pt] = (g.act_frac == kActAutoFrac) ? act_frac_of(m, g.a) : g.act_frac;
         bars.xs[pt] = 0;
     }
-    asm volatile("bar.sync 5, 384;" ::: "memory");
+    asm volatile("bar.sync 5, 128;" ::: "memory");
+    if TLP(g) tfb = gtimer();
     // ---- a1 (part 2) + a2 for the first chunk: cast, ballot-transpose (x_q fits 32 bits:
     // a <= 32), e2m1 B rows; two items per step keep two independent chains in flight
     auto transpose2 = [&](long long q0, long long q1, uint32_t& m0, uint32_t& m1) {
@@ -431,29 +471,45 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         if (b == B - 1)
             for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand(bstage0, NPAD, wl, n, 0u);
     };
-    auto chunk_pair = [&](int ia, float va, int ib, float vb) {
-        uint32_t ma, mb;
-        transpose2(act_cast(va, bars.f[ia < nci ? ia / kChunkWords : 0], g.a),
-                   act_cast(vb, bars.f[ib < nci ? ib / kChunkWords : 0], g.a), ma, mb);
-        if (ia < nci) put0(ia, ma);
-        if (ib < nci) put0(ib, mb);
-    };
+    // kCx items (itb + kPW * k) per step: kCx independent ballot chains in flight
+    auto chunk_group = [&](int itb, const float (&v)[kCx]) {
+        uint32_t u[kCx], mm[kCx];
+#pragma unroll
+        for (int k = 0; k < kCx; ++k) {
+            const int it = itb + kPW * k;
+            u[k] = (uint32_t)act_cast(v[k], bars.f[it < nci ? it / kChunkWords : 0], g.a);
+            mm[k] = 0;
+        }
 #pragma unroll 1
-    for (int it = pw, k = 0; it < nci; it += 2 * kPW, k += 2) {
-        const float va = k == 0 ? cx[0] : (k == 2 ? cx[2] : chunk_x(it));
-        const float vb = k == 0 ? cx[1] : chunk_x(it + kPW);
-        chunk_pair(it, va, it + kPW, vb);
+        for (int j = 0; j < g.a; ++j) {
+            const uint32_t bit = 1u << (g.a - 1 - j);
+#pragma unroll
+            for (int k = 0; k < kCx; ++k) {
+                const uint32_t w = __ballot_sync(0xffffffffu, (u[k] & bit) != 0);
+                if (lane == j) mm[k] = w;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kCx; ++k)
+            if (itb + kPW * k < nci) put0(itb + kPW * k, mm[k]);
+    };
+    chunk_group(pw, cx);                               // warp-uniform bounds (ballots inside)
+#pragma unroll 1
+    for (int itb = pw + kPW * kCx; itb < nci; itb += kPW * kCx) {
+        float v[kCx];
+#pragma unroll
+        for (int k = 0; k < kCx; ++k) v[k] = chunk_x(itb + kPW * k);
+        chunk_group(itb, v);
     }
+    if TLP(g) tcg = gtimer();
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA operand reads
-    asm volatile("bar.sync 5, 384;" ::: "memory");
+    asm volatile("bar.sync 5, 128;" ::: "memory");
     if (pt == 0) {
         mbar_arrive(&bars.b_full[0]);
-        if (p.dbg == 9) mbar_arrive(&bars.pro_done);
+        mbar_arrive(&bars.pro_done);
     }
     if TLP(g) tc0 = gtimer();
-    if (ew < 0) return;                                // the converters go on to convert
-    // ---- the CTA's slice of the grid-wide B operand (epilogue warps, bar 1; idle until
-    // their first segment)
+    // ---- the CTA's slice of the grid-wide B operand
     int k = 0;
 #pragma unroll 1
     for (uint32_t it = i0 + ew; it < i1; it += kEpiWarps, ++k) {
@@ -472,7 +528,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         if (lane == 0) atomicAdd(&bars.xs[b], (unsigned long long)xs);
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    const int et = pt - 32 * kConvWarps;
+    const int et = pt;
     if (et < B) {
         g.xsum[(int64_t)et * kXsumStride + blockIdx.x] = (long long)bars.xs[et];
         if (blockIdx.x == 0) g.f[et] = bars.f[et];
@@ -484,7 +540,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     if (TLP(g) && et == 0) {
         long long* r = tl_record(TLP(g));
         if (r) {
-            const long long rec[10] = {2, blockIdx.x, 0, 0, tpw, tmax, tc0, ttr, 0, 0};
+            const long long rec[10] = {2, blockIdx.x, 0, 0, tpw, tmax, tc0, ttr, tfb, tcg};
             for (int q = 0; q < 10; ++q) r[q] = rec[q];
         }
     }
@@ -519,7 +575,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     constexpr int kQConsumers = 2 + kConvWarps + kEpiWarps;   // warps 1, 2, converters, epilogue
     uint8_t* wtile0 = smem + kHdrBytes;
     uint8_t* btile0 = wtile0 + p.wstages * kWTileBytes;
-    unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(btile0 + 2 * kBStage);  // [b][128]
+    const uint32_t s_tot_s = smem_u32(btile0 + p.bstages * kBStage);   // [b][128] u64 (B > 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long G = gridDim.x;
@@ -535,9 +591,11 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             mbar_init(&bars.w_full[s], 1);
             mbar_init(&bars.w_empty[s], 4);              // the h-set that converts the tile
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < p.bstages; ++s) {
             mbar_init(&bars.b_full[s], 1);
             mbar_init(&bars.b_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mbar_init(&bars.d_full[s], 1);
             mbar_init(&bars.d_empty[s], kEpiWarps);
         }
@@ -596,7 +654,6 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         long long item = blockIdx.x;
         bool waited = false;
         int tc = 0;
-        if (p.dbg == 9 && g.x) mbar_wait(&bars.pro_done, 0);
         while (true) {
             mbar_wait(&bars.q_empty[qi], qph ^ 1);
             const long long u0 = item < p.items ? item * p.Gu : -1;
@@ -659,20 +716,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         auto wait_published = [&]() {
             if (g.x && !published) {
                 mbar_wait(&bars.slice_done, 0);                        // this CTA's slice is written
+                // the CTA's slice writes are ordered before the arrival by the epilogue warps'
+                // bar.sync + slice_done mbarrier and the cumulative release of the arrival
                 if (lane == 0) {
-                    // generation-based grid barrier; the arrival count is left zero.  The
-                    // CTA's writes are ordered before the arrival by bar.sync + this
-                    // cumulative fence.
-                    __threadfence();
-                    const int old = atomicAdd(g.gbar, 1);
-                    if (old == (int)G - 1) {
-                        __threadfence();
-                        atomicAdd(g.gbar + 1, 1);             // release the waiters first ...
-                        atomicExch(g.gbar, 0);                // ... then clear the count
-                    }
+                    grid_arrive(g.gbar);
+                    grid_wait(g.gbar, bars.gbase);
                 }
                 __syncwarp();
-                while (ld_acquire_gpu(g.gbar + 1) == bars.gen) __nanosleep(32);   // every CTA has arrived
                 asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> bulk-copy reads
                 if (TLP(g) && lane == 0) bars.t_b = gtimer();
                 // sum_c x_q[b, c] from every CTA's partial, for the epilogue
@@ -700,8 +750,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 if (g.x && cc == 0) continue;                 // built in place by the converters
                 wait_published();
                 const int kc = u % p.chunks;
-                const int st = cc & 1;
-                mbar_wait(&bars.b_empty[st], (uint32_t)(((cc >> 1) & 1) ^ 1));
+                const int st = cc % p.bstages;
+                mbar_wait(&bars.b_empty[st], (uint32_t)(((cc / p.bstages) & 1) ^ 1));
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&bars.b_full[st], kBStage);
                     bulk_g2s(btile0 + st * kBStage, g.bexp + (int64_t)kc * kBStage, kBStage, &bars.b_full[st]);
@@ -733,8 +783,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(p.d_col + db * p.regions * NPAD);
                 for (const int us = u; u < ue; ++u, ++cc) {
-                    const int st = cc & 1;
-                    TWAIT(&bars.b_full[st], (uint32_t)((cc >> 1) & 1), 1);
+                    const int st = cc % p.bstages;
+                    TWAIT(&bars.b_full[st], (uint32_t)((cc / p.bstages) & 1), 1);
                     tc_fence_after();
                     const uint64_t bdesc0 = b_desc(smem_u32(btile0 + st * kBStage));
                     for (int ps = 0; ps < p.passes; ++ps) {
@@ -784,9 +834,6 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         const uint32_t wtile_s = smem_u32(wtile0) + (uint32_t)m * 128;
         const uint32_t swz = (uint32_t)(m & 7);
-        if (g.x)
-            fused_prologue<NPAD>(g, p, bars, threadIdx.x - kConv0 * 32, btile0,
-                                 (int)(((long long)blockIdx.x * p.Gu) % p.chunks));
         int tc = 0, pc = 0;
         // passes in issue order; h-set h converts passes pc = h, h + 2, ...; pass pc uses A slot
         // pc % slots; its tiles are tc and tc + 1 (a stored pair) or tc alone
@@ -794,6 +841,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // software pipeline: a pass's TMEM stores drain while the next pass's tiles are awaited
         int pend_slot = -1;
         int npub = 0;
+        bool hold = g.x != nullptr, converted = false;
         auto publish = [&]() {
             if (pend_slot >= 0) {
                 tmem_st_wait();
@@ -822,6 +870,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     if (stored_pair) TWAIT(&bars.w_full[st1], (uint32_t)(((tc + 1) / p.wstages) & 1), 3);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[1] = gtimer();
                     publish();                          // previous pass's A is in TMEM: tell the MMA
+                    if (hold && pend_slot < 0 && converted) {   // this h-set's first pass is published
+                        // fused path: after its first pass an h-set waits for the prologue (the
+                        // epilogue warps' x wave and first B chunk), which it would otherwise
+                        // slow down by competing for issue slots; the MMAs need both anyway
+                        mbar_wait(&bars.pro_done, 0);
+                        hold = false;
+                    }
                     TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
                     tc_fence_after();
                     const int kind = stored_pair ? (use_lo ? 0 : 1) : 2;
@@ -839,6 +894,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         convert_pass<2>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
                     tc += ntile;
+                    converted = true;
                     pend_slot = slot;
                     slot += 2;
                     while (slot >= p.slots) {
@@ -885,10 +941,12 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             g.y[o] = apply_fn(yv, g.fn);
         };
         if (g.x)
-            fused_prologue<NPAD>(g, p, bars, threadIdx.x - kConv0 * 32, btile0,
+            fused_prologue<NPAD>(g, p, bars, threadIdx.x - kEpi0 * 32, btile0,
                                  (int)(((long long)blockIdx.x * p.Gu) % p.chunks));
         else
             pdl_wait();
+        // end-of-work barrier base (after the PDL wait above: every earlier call is complete)
+        const unsigned long long ebase = (ew == 0 && lane == 0) ? grid_base(g.ebar) : 0ull;
         int seg = 0;
         while (true) {
             const int2 it = take_item(bars, qi, qph, lane);
@@ -901,29 +959,49 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 const int db = seg & 1;
                 mbar_wait(&bars.d_full[db], (uint32_t)((seg >> 1) & 1));
                 tc_fence_after();
-                long long te[3] = {0, 0, 0};
-                if TLP(g) te[0] = gtimer();
-                // tot_b = sum_j T_j sum_r |S_lo(r)| D_r[b*a + j]; lo(r) = least significant layer of group r
+                long long te[4] = {0, 0, 0, 0}, tcy[3] = {0, 0, 0};
+                if TLP(g) {
+                    te[0] = gtimer();
+                    tcy[0] = clock64();
+                }
+                // tot_b = sum_r |S_lo(r)| sum_j T_j D_r[b*a + j]; lo(r) = least significant layer of group
+                // r.  The plane sum runs as Horner's rule (T_0 = -2^(a-1), T_j = 2^(a-1-j)):
+                // h = -D[0]; h = 2h + D[j] -- branch-free, exact modulo 2^64.  B = 1 keeps the
+                // total in a register; B > 1 parks per-column totals in SMEM (s_tot).
+                unsigned long long tot1 = 0;
                 for (int r = 0; r < p.regions; ++r) {
                     int last = (r + 1) * p.Gp - 1;
                     if (last > p.passes - 1) last = p.passes - 1;
                     const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
-                    unsigned long long acc = 0;
-                    int j = 0, bc = 0;
-#pragma unroll 1
-                    for (int c8 = 0; c8 < NPAD && bc < g.B; c8 += 8) {
-                        uint32_t dv[8];
-                        ld_tmem_x8(tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD + c8), dv);
-                        tmem_ld_wait();
+                    // all of the region's columns in one batch of loads, one wait
+                    uint32_t dv[NPAD];
+                    ld_tmem_cols<NPAD>(tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD), dv);
+                    tmem_ld_wait();
+                    if (TLP(g) && r == 0) {
+                        te[3] = gtimer();
+                        tcy[1] = clock64();
+                    }
+                    if (g.B == 1) {
+                        unsigned long long h = 0ull - (unsigned long long)__float2uint_rn(__uint_as_float(dv[0]));
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
+                        for (int e = 1; e < NPAD; ++e) {
+                            const unsigned long long v = (unsigned long long)__float2uint_rn(__uint_as_float(dv[e]));
+                            h = (e < g.a) ? h + h + v : h;
+                        }
+                        tot1 += h * wr;
+                    } else {
+                        unsigned long long h = 0;
+                        int j = 0, bc = 0;
+#pragma unroll
+                        for (int e = 0; e < NPAD; ++e) {
                             if (bc < g.B) {
-                                acc += plane_scale(g.a, j) *
-                                       (wr * (unsigned long long)__float2uint_rn(__uint_as_float(dv[e])));
+                                const unsigned long long v =
+                                    (unsigned long long)__float2uint_rn(__uint_as_float(dv[e]));
+                                h = j == 0 ? 0ull - v : h + h + v;
                                 if (++j == g.a) {
-                                    if (r == 0) s_tot[bc * kTcRows + m] = acc;
-                                    else s_tot[bc * kTcRows + m] += acc;
-                                    acc = 0;
+                                    const uint32_t sa = s_tot_s + (uint32_t)(bc * kTcRows + m) * 8u;
+                                    const unsigned long long t = h * wr;
+                                    st_shared_u64(sa, r == 0 ? t : t + ld_shared_u64(sa));
                                     j = 0;
                                     ++bc;
                                 }
@@ -934,16 +1012,26 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.d_empty[db]);
-                if TLP(g) te[1] = gtimer();
+                if TLP(g) {
+                    te[1] = gtimer();
+                    tcy[2] = clock64();
+                }
                 // exact integer adds into the tile's accumulator (order-independent); no
                 // round trip here: tiles are finalised after the end-of-work grid barrier
                 unsigned long long* ab = g.accbuf + (int64_t)rt * g.B * kTcRows + m;
-                for (int b = 0; b < g.B; ++b) red_add_u64(ab + b * kTcRows, s_tot[b * kTcRows + m]);
+                if (g.B == 1)
+                    red_add_u64(ab, tot1);
+                else
+                    for (int b = 0; b < g.B; ++b)
+                        red_add_u64(ab + b * kTcRows, ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
                 if (TLP(g) && ew == 0 && lane == 0) {
                     te[2] = gtimer();
+                    bars.t_eseg[0] = te[0];
+                    bars.t_eseg[1] = te[1];
+                    bars.t_eseg[2] = te[2];
                     long long* rr = tl_record(TLP(g));
                     if (rr) {
-                        const long long rec[10] = {3, blockIdx.x, seg, kcB - kcA, te[0], te[1], te[2], te[2], 0, 0};
+                        const long long rec[10] = {3, blockIdx.x, seg, kcB - kcA, te[0], te[1], te[2], tcy[1] - tcy[0], te[3], tcy[2] - tcy[1]};
                         for (int k = 0; k < 10; ++k) rr[k] = rec[k];
                     }
                 }
@@ -951,21 +1039,14 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             }
         }
         // ---- end-of-work grid barrier (the 128 threads' adds are ordered before the arrival by
-        // bar.sync + thread 0's cumulative fence), then this CTA finalises tiles
+        // bar.sync + thread 0's cumulative release), then this CTA finalises tiles
         // blockIdx.x, blockIdx.x + G, ...: y from the exact tile sums, accumulators re-zeroed
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (ew == 0 && lane == 0) {
-            const int gen = ld_acquire_gpu(g.ebar + 1);
-            __threadfence();
-            const int old = atomicAdd(g.ebar, 1);
-            if (old == (int)G - 1) {
-                __threadfence();
-                atomicAdd(g.ebar + 1, 1);
-                atomicExch(g.ebar, 0);
-            } else {
-                while (ld_acquire_gpu(g.ebar + 1) == gen) __nanosleep(32);
-            }
-            __threadfence();
+            if TLP(g) bars.t_ebar[0] = gtimer();
+            grid_arrive(g.ebar);
+            grid_wait(g.ebar, ebase);                // acquire; bar.sync passes it to the CTA
+            if TLP(g) bars.t_ebar[1] = gtimer();
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (long long rt = blockIdx.x; rt < p.tiles; rt += G) {
@@ -999,6 +1080,12 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             const long long rec[10] = {1, blockIdx.x, smid, 0, g_start, bars.t_b, bars.t_mma0, bars.t_mend,
                                        bars.t_cend, gtimer()};
             for (int k = 0; k < 10; ++k) r[k] = rec[k];
+        }
+        long long* r6 = tl_record(TLP(g));
+        if (r6) {
+            const long long rec[10] = {6, blockIdx.x, bars.t_mend, bars.t_eseg[0], bars.t_eseg[1], bars.t_eseg[2],
+                                       bars.t_ebar[0], bars.t_ebar[1], bars.t_cend, gtimer()};
+            for (int k = 0; k < 10; ++k) r6[k] = rec[k];
         }
         long long* r5 = tl_record(TLP(g));
         if (r5) {
@@ -1087,7 +1174,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 {
     static int sms = 0;
     static bool attr = false;
-    static int dbg = -1, prof = 0;
+    static int dbg = -1, prof = 0, bst_env = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1096,6 +1183,8 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
         dbg = ev ? atoi(ev) : 0;
         ev = getenv("PB_TC_PROF");
         prof = ev ? atoi(ev) : 0;
+        ev = getenv("PB_TC_BSTAGES");          // experiment knob: B ring depth
+        bst_env = ev ? atoi(ev) : 0;
     }
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1113,7 +1202,9 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     p.dbg = dbg;
     p.prof = prof;
     // weight ring: every 16 KiB stage the B stages and epilogue sums leave free
-    const uint32_t fixed = 1024 + kHdrBytes + 2 * (kChunkWords / 2) * NPAD * 32 + (uint32_t)g.B * kTcRows * 8;
+    p.bstages = p.passes <= 2 ? kMaxBStages : 2;
+    if (bst_env) p.bstages = bst_env < 2 ? 2 : (bst_env > kMaxBStages ? kMaxBStages : bst_env);
+    const uint32_t fixed = 1024 + kHdrBytes + (uint32_t)p.bstages * (kChunkWords / 2) * NPAD * 32 + (uint32_t)g.B * kTcRows * 8;
     p.wstages = (int)((kSmemMax - fixed) / kWTileBytes);
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     if (p.wstages < 4) return cudaErrorNotSupported;

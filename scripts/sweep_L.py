@@ -1,0 +1,59 @@
+"""Quick us/call sweep over L (k_used = L) at one shape, weights rotating over
+>= 2x L2 (as bench.py), one CUDA graph per copy.  Experiment helper only.
+  python scripts/sweep_L.py --L 1 2 4 8 [--R 16384 --K 16384 --B 1 --a 16]"""
+import argparse
+import math
+
+import numpy as np
+import torch
+
+import paper_2003_00822_b200 as pb
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--R", type=int, default=16384)
+ap.add_argument("--K", type=int, default=16384)
+ap.add_argument("--B", type=int, default=1)
+ap.add_argument("--a", type=int, default=16)
+ap.add_argument("--L", type=int, nargs="+", default=[1, 2, 4, 8, 16])
+ap.add_argument("--steps", type=int, default=60)
+args = ap.parse_args()
+l2 = torch.cuda.get_device_properties(0).L2_cache_size
+x = torch.randn(args.B, args.K, device="cuda")
+y = torch.empty(args.B, args.R, device="cuda")
+ws = pb.Workspace(pb.workspace_bytes(args.B, args.K, args.a))
+rng = np.random.default_rng(1)
+s = torch.cuda.Stream()
+out = []
+for L in args.L:
+    if L == 1:
+        codes = (1 - 2 * rng.integers(0, 2, size=(args.R, args.K))).astype(np.int32)
+    else:
+        codes = rng.integers(-(1 << (L - 1)), 1 << (L - 1), size=(args.R, args.K), dtype=np.int32)
+    w0 = pb.PackedWeights.from_codes(codes, L, offset=1 if L == 1 else 0)
+    M = max(1, math.ceil(2 * l2 / w0.nbytes()))
+    cp = [w0] + [w0.clone_to(torch.empty_like(w0.buf)) for _ in range(M - 1)]
+    with torch.cuda.stream(s):
+        for w in cp:
+            pb.matmul(x, w, L, args.a, y=y, ws=ws, stream=s)
+    torch.cuda.synchronize()
+    gs = []
+    for w in cp:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            pb.matmul(x, w, L, args.a, y=y, ws=ws, stream=s)
+        gs.append(g)
+    for i in range(6):
+        gs[i % M].replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for i in range(args.steps):
+        gs[i % M].replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / args.steps
+    gbs = (L * args.R * args.K / 8 + 4 * args.B * (args.K + args.R)) / us / 1e3
+    out.append(f"L={L}:{us:.1f}us/{gbs:.0f}GB/s")
+    del gs, cp, w0
+    torch.cuda.empty_cache()
+print(f"R={args.R} K={args.K} B={args.B} a={args.a}  " + "  ".join(out), flush=True)

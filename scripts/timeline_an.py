@@ -38,6 +38,9 @@ if len(pr):
         print(f"prologue call {c}: pdl-wait done {f(q[:,4]).min():8.2f}..{f(q[:,4]).max():8.2f}  "
               f"max done {f(q[:,5]).min():8.2f}..{f(q[:,5]).max():8.2f}  chunk0 done {f(q[:,6]).min():8.2f}..{f(q[:,6]).max():8.2f}  "
               f"slice done {f(q[:,7]).min():8.2f}..{f(q[:,7]).max():8.2f}")
+        if q[:, 8].any():
+            print(f"   max->f_b med {np.median(q[:,8]-q[:,5])/1e3:.2f}  f_b->groups done med {np.median(q[:,9]-q[:,8])/1e3:.2f}"
+                  f"  groups->chunk0 published med {np.median(q[:,6]-q[:,9])/1e3:.2f} us")
 ep = rec[rec[:, 0] == 3]
 if len(ep):
     # per epilogue segment: d_full wake -> TMEM drained -> slot/atomic done -> y stored
@@ -45,6 +48,10 @@ if len(ep):
     d1 = (ep[:, 5] - ep[:, 4]) / 1e3
     d2 = (ep[:, 6] - ep[:, 5]) / 1e3
     d3 = (ep[:, 7] - ep[:, 6]) / 1e3
+    if ep[:, 8].any():
+        dl = (ep[:, 8] - ep[:, 4]) / 1e3
+        print(f"epilogue: wake -> TMEM loads done med {np.median(dl):.2f} max {dl.max():.2f} us; cycles: loads med "
+              f"{np.median(ep[:,7]):.0f}, math+release med {np.median(ep[:,9]):.0f} max {ep[:,9].max():.0f}")
     print(f"epilogue segments {len(ep)}: TMEM->s_tot med {np.median(d1):.2f} max {d1.max():.2f} us; "
           f"slot+atomic med {np.median(d2):.2f} max {d2.max():.2f}; final med {np.median(d3):.2f} max {d3.max():.2f}")
     for kind, name in ((1, "whole"), (2, "finalizer"), (0, "parker")):
@@ -82,3 +89,15 @@ if len(fp):
         q = fp[c * ncta:(c + 1) * ncta]
         print(f"chunk0 call {c}: x issued {f(q[:,2]).min():8.2f}..{f(q[:,2]).max():8.2f}  f ready {f(q[:,3]).min():8.2f}..{f(q[:,3]).max():8.2f}"
               f"  built {f(q[:,8]).min():8.2f}..{f(q[:,8]).max():8.2f}  (build med {np.median((q[:,8]-q[:,3])/1e3):.2f} us)")
+t6 = rec[rec[:, 0] == 6]
+if len(t6):
+    t6 = t6[np.argsort(t6[:, 2], kind="stable")]
+    for c in range(len(t6) // ncta):
+        q = t6[c * ncta:(c + 1) * ncta]
+        base = q[:, 2].max()                      # the last CTA's MMA end
+        rel = lambda col: (q[:, col] - base) / 1e3
+        print(f"tail call {c} (us after the LAST mend): mend spread {(q[:,2].max()-q[:,2].min())/1e3:.2f}; "
+              f"last seg wake med {np.median(rel(3)):.2f} max {rel(3).max():.2f}; drained med {np.median(rel(4)):.2f} "
+              f"max {rel(4).max():.2f}; added max {rel(5).max():.2f}; bar arrive max {rel(6).max():.2f}; "
+              f"bar exit med {np.median(rel(7)):.2f} max {rel(7).max():.2f}; fin med {np.median(rel(8)):.2f} "
+              f"max {rel(8).max():.2f}; end max {rel(9).max():.2f}")
