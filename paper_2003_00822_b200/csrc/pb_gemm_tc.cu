@@ -779,7 +779,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 int ue = (rt + 1) * p.chunks;
                 if (ue > it.y) ue = it.y;
                 const int db = seg & 1;
-                if (seg >= 2) mbar_wait(&bars.d_empty[db], (uint32_t)(((seg >> 1) - 1) & 1));
+                if (seg >= 2) TWAIT(&bars.d_empty[db], (uint32_t)(((seg >> 1) - 1) & 1), 0);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(p.d_col + db * p.regions * NPAD);
                 for (const int us = u; u < ue; ++u, ++cc) {

@@ -73,6 +73,8 @@ if len(pf):
             continue
         tot = np.median(q[:, 3]) / 1e3
         nm = names if w < 3 else ["convert", "st_wait"] + names[2:]
+        if w == 1:
+            nm = ["d_empty"] + names[1:]
         parts = "  ".join(f"{n} {np.median(q[:, 4 + i]) / 1e3:6.2f}" for i, n in enumerate(nm) if q[:, 4 + i].any())
         print(f"  warp {w:2d}: total {tot:6.2f} us  waits(med, us): {parts}")
 

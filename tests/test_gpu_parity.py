@@ -201,7 +201,11 @@ def test_latency_drops_with_fewer_layers(pb, torch):
 
 @pytest.mark.parametrize("R,K,B,L,k_used,a", [(1024, 8192, 1, 4, 4, 16), (1000, 3000, 2, 8, 5, 16),
                                               (300, 4096, 4, 3, 3, 8), (129, 1000, 1, 16, 16, 16),
-                                              (2048, 2048, 1, 8, 8, 32), (640, 6000, 3, 2, 2, 5)])
+                                              (2048, 2048, 1, 8, 8, 32), (640, 6000, 3, 2, 2, 5),
+                                              # many units per CTA (dynamic claims), two accumulator
+                                              # groups (L=16, K=8192: 5 passes per group), batch columns
+                                              (4096, 8192, 1, 8, 8, 16), (4000, 8192, 1, 16, 11, 16),
+                                              (8192, 8192, 1, 4, 4, 16), (4096, 8100, 3, 6, 5, 8)])
 def test_tc_streamk_repeat(pb, torch, orc, R, K, B, L, k_used, a):
     # tensor engine: stream-K partial tiles + self-cleaning scratch across calls
     s = synth.seed(2, 3000 + R + K)
