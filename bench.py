@@ -240,7 +240,7 @@ def main():
 
     def rotation(w):
         nb = w.nbytes()
-        M = max(1, math.ceil(2 * l2 / max(nb, 1)))
+        M = max(2, math.ceil(2 * l2 / max(nb, 1)))     # >= 2: consecutive calls never share weights
         copies = [w] + [w.clone_to(torch.empty_like(w.buf)) for _ in range(M - 1)]
         return copies
 
@@ -261,19 +261,31 @@ def main():
         else:
             pb.matmul(x, w, k_used, a, y=y, ws=ws, stream=s)
 
-    def capture(ws_list, fn):
-        graphs = []
+    def capture(ws_list, fn, steps):
+        """Graphs of consecutive calls cycling over the weight copies (the paper times
+        1000 back-to-back iterations): a main graph of `per` calls and, when
+        `steps` is not a multiple of it, a remainder graph, so a timed region replays
+        exactly `steps` calls.  Within a graph the calls are chained by the kernel's
+        programmatic (PDL) launch edges, as in any multi-layer pipeline."""
+        M = len(ws_list)
+        per = M * max(1, 8 // M) if M <= 8 else M
+        per = max(1, min(per, steps))
         with torch.cuda.stream(stream):
             for w in ws_list:          # warm (sets kernel attributes outside capture)
                 fn(w, stream)
         torch.cuda.synchronize()
-        for w in ws_list:
+
+        def graph_of(n):
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=stream):
-                fn(w, stream)
-            graphs.append(g)
+                for t in range(n):
+                    fn(ws_list[t % M], stream)
+            return g
+        plan = {"per": per, "main": graph_of(per), "rem": None, "n_rem": steps % per}
+        if plan["n_rem"]:
+            plan["rem"] = graph_of(plan["n_rem"])
         torch.cuda.synchronize()
-        return graphs
+        return plan
 
     def barrier():
         torch.cuda.synchronize()
@@ -288,19 +300,24 @@ def main():
         dist.all_reduce(t, dist.ReduceOp.MAX)
         return t.item()
 
-    def time_graphs(graphs, steps, warmup):
-        for i in range(warmup):
-            graphs[i % len(graphs)].replay()
+    def time_graphs(plan, steps, warmup):
+        """Device time (ms, max over ranks) of exactly `steps` calls from `plan`."""
+        per = plan["per"]
+        for _ in range(-(-warmup // per)):
+            plan["main"].replay()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for i in range(steps):
-            graphs[i % len(graphs)].replay()
+        for _ in range(steps // per):
+            plan["main"].replay()
+        if steps % per:
+            assert plan["n_rem"] == steps % per
+            plan["rem"].replay()
         e1.record()
         barrier()
         return max_over_ranks(e0.elapsed_time(e1))
 
-    graphs = capture(copies, step)
+    graphs = capture(copies, step, args.steps)
 
     # ---- headline: K steps, device-timed, max over ranks, clocks sampled
     idx = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0" \
@@ -350,6 +367,15 @@ def main():
     second_ms = max_over_ranks(statistics.mean(e[1].elapsed_time(e[2]) for e in ev))
     gemv_ms, act_ms = (first_ms, 0.0) if fused else (second_ms, first_ms)
     gemv_bytes = k_used * rs * K / 8          # algorithmic bytes per GEMV launch (this rank)
+    # When every launch in the headline's timed region is the dominant kernel (fused engine,
+    # one launch per call, no collective), its average launch duration is that region's
+    # event time / launches -- measured on the stream the graphs replay on, back to back
+    # as in the step.  Otherwise (and always reported): each launch bracketed by its own
+    # events, serialised (no PDL overlap with its neighbours).
+    in_region = fused and launches_per_call == 1 and N == 1
+    iso_ms = gemv_ms
+    if in_region:
+        gemv_ms = ms_step
     achieved = gemv_bytes / (gemv_ms * 1e-3) / 1e9
     peak, peak_src = measured_peaks()
     traffic = None
@@ -365,28 +391,60 @@ def main():
                 "kernel": "bitgemm_tc_kernel (fused a1-a5)" if fused else "bitgemv_popc_kernel (a3-a5)",
                 "peak_source": peak_src, "algorithmic_bytes_per_launch": gemv_bytes,
                 "avg_launch_us": gemv_ms * 1e3, "act_kernel_us": act_ms * 1e3,
+                "launch_timing": ("events around the timed region / launches (all launches are this kernel)"
+                                  if in_region else "events around each launch"),
+                "isolated_launch_us": iso_ms * 1e3,
                 "kernel_share_of_step": gemv_ms / ms_step}
 
-    # ---- e2e through the public API with host buffers (pinned), per step:
-    #      H2D x, pb matmul, D2H y.
-    y_h = torch.empty((B, R), dtype=torch.float32).pin_memory()
-    for i in range(3):
-        x.copy_(x_h, non_blocking=True)
-        step(copies[i % M])
-        y_h.copy_(y, non_blocking=True)
+    # ---- e2e through the public API with host buffers (pinned), per step: H2D of that
+    #      step's x, pb matmul, D2H of its y.  Serving-style pipeline: copies run on their
+    #      own streams, double-buffered, so step i's D2H and step i+1's H2D overlap the
+    #      kernels (event-ordered; every step still moves its own bytes both ways).
+    cs = torch.cuda.current_stream()
+    h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+    xb = [torch.empty_like(x) for _ in range(2)]
+    yb = [torch.empty_like(y) for _ in range(2)]
+    y_hb = [torch.empty((B, R), dtype=torch.float32).pin_memory() for _ in range(2)]
+    ev_h2d = [torch.cuda.Event() for _ in range(2)]
+    ev_k = [torch.cuda.Event() for _ in range(2)]
+    ev_d2h = [torch.cuda.Event() for _ in range(2)]
+
+    def e2e_step(i):
+        j = i & 1
+        with torch.cuda.stream(h2d_s):
+            if i >= 2:
+                h2d_s.wait_event(ev_k[j])               # kernel i-2 is done reading xb[j]
+            xb[j].copy_(x_h, non_blocking=True)
+            ev_h2d[j].record(h2d_s)
+        cs.wait_event(ev_h2d[j])
+        if i >= 2:
+            cs.wait_event(ev_d2h[j])                    # y of step i-2 has left yb[j]
+        if N > 1:
+            pb.matmul_rowshard(xb[j], copies[i % M], R, comm, k_used, a, y_full=yb[j], ws=ws, stream=cs)
+        else:
+            pb.matmul(xb[j], copies[i % M], k_used, a, y=yb[j], ws=ws, stream=cs)
+        ev_k[j].record(cs)
+        with torch.cuda.stream(d2h_s):
+            d2h_s.wait_event(ev_k[j])
+            y_hb[j].copy_(yb[j], non_blocking=True)
+            ev_d2h[j].record(d2h_s)
+
+    for i in range(4):
+        e2e_step(i)
     barrier()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record()
+    e0.record(cs)
+    h2d_s.wait_event(e0)
     for i in range(args.steps):
-        x.copy_(x_h, non_blocking=True)
-        step(copies[i % M])
-        y_h.copy_(y, non_blocking=True)
-    e1.record()
+        e2e_step(i)
+    cs.wait_stream(d2h_s)
+    e1.record(cs)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     e2e = {"value": bytes_step / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
            "h2d_bytes_per_step": 4 * B * K, "d2h_bytes_per_step": 4 * B * R,
-           "api": "paper_2003_00822_b200.matmul%s (ctypes -> C ABI), host pinned x/y" %
+           "api": "paper_2003_00822_b200.matmul%s (ctypes -> C ABI), pinned host x/y, copies on "
+                  "their own streams, double-buffered" %
                   ("_rowshard" if N > 1 else "")}
 
     # ---- sweeps (single GPU): per stored bitlayers L = 1..16 and per k_used
@@ -396,14 +454,15 @@ def main():
         for Lx in range(1, 17):
             wx = pack(Lx)
             cx = rotation(wx)
-            gx = capture(cx, lambda w, s: pb.matmul(x, w, Lx, a, y=y, ws=ws, stream=s))
+            gx = capture(cx, lambda w, s: pb.matmul(x, w, Lx, a, y=y, ws=ws, stream=s), args.sweep_steps)
             t = time_graphs(gx, args.sweep_steps, 3) / args.sweep_steps
             gbs = algo_bytes(R, K, B, Lx) / (t * 1e-3) / 1e9
             per_L.append({"L": Lx, "k_used": Lx, "us_per_call": t * 1e3, "GBps": gbs, "frac_of_peak": gbs / peak,
                           "frac_of_8TBps": gbs / 8000.0, "copies": len(cx)})
             if Lx == 16:
                 for k in (16, 12, 8, 4, 2, 1):
-                    gk = capture(cx, lambda w, s, k=k: pb.matmul(x, w, k, a, y=y, ws=ws, stream=s))
+                    gk = capture(cx, lambda w, s, k=k: pb.matmul(x, w, k, a, y=y, ws=ws, stream=s),
+                                 args.sweep_steps)
                     tk = time_graphs(gk, args.sweep_steps, 3) / args.sweep_steps
                     per_k.append({"L": 16, "k_used": k, "us_per_call": tk * 1e3,
                                   "GBps": algo_bytes(R, K, B, k) / (tk * 1e-3) / 1e9})
