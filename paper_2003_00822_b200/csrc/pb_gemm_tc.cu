@@ -371,10 +371,11 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 //      L2-resident B*K floats), plus the values of the CTA's first chunk and of
 //      its slice of the grid-wide B operand;
 //   2. f_b (reading G8);
-//   3. the CTA's first chunk kc0 of B, built straight into B stage 0, so the
-//      first MMAs wait neither for the grid barrier nor a copy;
-//   4. the CTA's 1/G slice of the (b, word) items of B into the workspace tiles
-//      + its sum of x_q, published by warp 2's grid barrier.
+//   3. the CTA's 1/G slice of the (b, word) items of B into the workspace tiles
+//      + its sum of x_q, published by warp 2's grid barrier (which then runs
+//      while step 4 does);
+//   4. the CTA's first chunk kc0 of B, built straight into B stage 0, so the
+//      first MMAs wait neither for the grid barrier nor a copy.
 template <int NPAD>
 __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& p, Bars& bars, int pt,
                                                uint8_t* bstage0, int kc0) {
@@ -450,8 +451,6 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     }
     asm volatile("bar.sync 5, 128;" ::: "memory");
     if TLP(g) tfb = gtimer();
-    // ---- a1 (part 2) + a2 for the first chunk: cast, ballot-transpose (x_q fits 32 bits:
-    // a <= 32), e2m1 B rows; two items per step keep two independent chains in flight
     auto transpose2 = [&](long long q0, long long q1, uint32_t& m0, uint32_t& m1) {
         const uint32_t u0 = (uint32_t)q0, u1 = (uint32_t)q1;
         m0 = m1 = 0;
@@ -465,6 +464,37 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
             }
         }
     };
+    // ---- the CTA's slice of the grid-wide B operand first: warp 2's grid barrier that
+    // publishes the slices for the later chunks then overlaps the first chunk's build
+    int k = 0;
+#pragma unroll 1
+    for (uint32_t it = i0 + ew; it < i1; it += kEpiWarps, ++k) {
+        const uint32_t b = it / Wt;
+        const uint32_t w = it - b * Wt;
+        const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
+        const long long q = act_cast(v, bars.f[b], g.a);
+        uint32_t mine, dummy;
+        transpose2(q, 0, mine, dummy);
+        if (lane < g.a) put_b_operand(g.bexp, NPAD, w, b * g.a + lane, mine);
+        if (b == B - 1)
+            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand(g.bexp, NPAD, w, n, 0u);
+        long long xs = q;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+        if (lane == 0) atomicAdd(&bars.xs[b], (unsigned long long)xs);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int et = pt;
+    if (et < B) {
+        g.xsum[(int64_t)et * kXsumStride + blockIdx.x] = (long long)bars.xs[et];
+        if (blockIdx.x == 0) g.f[et] = bars.f[et];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if TLP(g) ttr = gtimer();
+    // warp 2 arrives at the grid barrier for this CTA once its slice is written
+    if (et == 0) mbar_arrive(&bars.slice_done);
+    // ---- a1 (part 2) + a2 for the first chunk: cast, ballot-transpose (x_q fits 32 bits:
+    // a <= 32), e2m1 B rows straight into B stage 0
     auto put0 = [&](int it, uint32_t mine) {
         const int b = it / kChunkWords, wl = it - b * kChunkWords;
         if (lane < g.a) put_b_operand(bstage0, NPAD, wl, b * g.a + lane, mine);
@@ -509,34 +539,6 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         mbar_arrive(&bars.pro_done);
     }
     if TLP(g) tc0 = gtimer();
-    // ---- the CTA's slice of the grid-wide B operand
-    int k = 0;
-#pragma unroll 1
-    for (uint32_t it = i0 + ew; it < i1; it += kEpiWarps, ++k) {
-        const uint32_t b = it / Wt;
-        const uint32_t w = it - b * Wt;
-        const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
-        const long long q = act_cast(v, bars.f[b], g.a);
-        uint32_t mine, dummy;
-        transpose2(q, 0, mine, dummy);
-        if (lane < g.a) put_b_operand(g.bexp, NPAD, w, b * g.a + lane, mine);
-        if (b == B - 1)
-            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand(g.bexp, NPAD, w, n, 0u);
-        long long xs = q;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
-        if (lane == 0) atomicAdd(&bars.xs[b], (unsigned long long)xs);
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    const int et = pt;
-    if (et < B) {
-        g.xsum[(int64_t)et * kXsumStride + blockIdx.x] = (long long)bars.xs[et];
-        if (blockIdx.x == 0) g.f[et] = bars.f[et];
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if TLP(g) ttr = gtimer();
-    // warp 2 arrives at the grid barrier for this CTA once its slice is written
-    if (et == 0) mbar_arrive(&bars.slice_done);
     if (TLP(g) && et == 0) {
         long long* r = tl_record(TLP(g));
         if (r) {
@@ -870,7 +872,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     if (stored_pair) TWAIT(&bars.w_full[st1], (uint32_t)(((tc + 1) / p.wstages) & 1), 3);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[1] = gtimer();
                     publish();                          // previous pass's A is in TMEM: tell the MMA
-                    if (hold && pend_slot < 0 && converted) {   // this h-set's first pass is published
+                    if (hold && pend_slot < 0 && (converted || p.dbg == 11)) {   // this h-set's first pass is published
                         // fused path: after its first pass an h-set waits for the prologue (the
                         // epilogue warps' x wave and first B chunk), which it would otherwise
                         // slow down by competing for issue slots; the MMAs need both anyway
