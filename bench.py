@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--sweep-steps", type=int, default=40)
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="oracle cpu_baseline budget")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline (profiling runs)")
+    p.add_argument("--no-compare", action="store_true", help="skip the cuBLAS fp32/bf16/int8 comparison (f3)")
     p.add_argument("--ref-budget", type=float, default=120.0, help="--impl reference total budget (s)")
     return p.parse_args()
 
@@ -470,6 +471,38 @@ def main():
             del gx, cx, wx
             torch.cuda.empty_cache()
 
+    # ---- comparison systems on the same B200 (context, not target): the
+    #      dense matvec at the same shape through cuBLAS in fp32 and bf16, and int8 via
+    #      torch._int_mm (cuBLASLt; its m > 16 rule pads the batch to 32 columns).  Same
+    #      protocol as ours: rotating weight copies >= 2x L2, graphs of back-to-back calls.
+    compare = None
+    if not args.no_compare and N == 1:
+        compare = {"note": "cuBLAS at the same R x K and batch; speedup = their us / ours (the paper's "
+                           "Table 1 framing, P:218-247); context, not target", "systems": {}}
+        xs = torch.randn(K, B, device="cuda")
+        for name, dt in (("fp32", torch.float32), ("bf16", torch.bfloat16), ("int8", torch.int8)):
+            try:
+                esz = torch.tensor([], dtype=dt).element_size()
+                Mc = max(2, math.ceil(2 * l2 / (R * K * esz)))
+                if dt == torch.int8:
+                    Ws = [torch.randint(-127, 128, (K, R), dtype=dt, device="cuda") for _ in range(Mc)]
+                    xin = torch.randint(-127, 128, (max(32, B), K), dtype=dt, device="cuda")
+                    fn = lambda Wc: torch._int_mm(xin, Wc)
+                else:
+                    Ws = [torch.randn(R, K, device="cuda").to(dt) for _ in range(Mc)]
+                    xin = xs.to(dt)
+                    fn = lambda Wc: torch.matmul(Wc, xin)
+                cp = capture(Ws, lambda Wc, s_: fn(Wc), args.sweep_steps)
+                tc = time_graphs(cp, args.sweep_steps, 3) / args.sweep_steps
+                ent = {"us_per_call": tc * 1e3, "GBps": R * K * esz / (tc * 1e-3) / 1e9, "weight_copies": Mc}
+                ent["pb_speedup_at_L"] = {str(r["L"]): tc * 1e3 / r["us_per_call"] for r in per_L} if per_L \
+                    else {str(L): tc / ms_step}
+                compare["systems"][name] = ent
+                del cp, Ws
+                torch.cuda.empty_cache()
+            except Exception as e:      # comparison only: report, never fail the bench
+                compare["systems"][name] = {"error": str(e)[:200]}
+
     # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
@@ -499,7 +532,7 @@ def main():
                                  f"{M * w0.nbytes() / 2**20:.0f} MiB >= 2x L2 ({l2 / 2**20:.0f} MiB)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": (launches_per_call + (1 if (N > 1 and B > 1) else 0)) * args.steps,
-                "clocks": clocks, "per_L": per_L, "per_kused": per_k,
+                "clocks": clocks, "per_L": per_L, "per_kused": per_k, "compare": compare,
                 "context": "paper: >8x end-to-end vs FP32 on a Tesla T4 (P:28, P:216) -- context, not target"}
         print(json.dumps(line), flush=True)
     if N > 1:

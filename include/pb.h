@@ -145,7 +145,8 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
  *   [work counters int32 x 2]                 zero on entry, left zero
  *   [end barrier int32 x 2]                   arrival count (zero on entry,
  *                                             left zero) + generation
- *   [tensor-engine partial-tile sums int64 x 2048 x batch x 128]
+ *   [tensor-engine partial-tile sums int64 x 2048 x S x 128, S = the largest
+ *    batch slice of one launch for this act_bits, min(32, 64 / act_bits)]
  *                                             zero on entry, left zero
  *   [f_b int32 x batch][x_q partial sums int64 x batch x 160]
  *   [planes uint32 x batch x act_bits x kwords]
@@ -153,7 +154,9 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
  *    padded to 8/16/32, present when a*batch <= 32]
  * each region 256-byte aligned.  The workspace must be zero-filled before its
  * first use (the counters); every other region is rewritten by each call, so
- * one workspace serves calls of any shape, but not two calls concurrently.
+ * one workspace serves calls of any shape with the same act_bits (the
+ * partial-tile sums sit at the same place for all of them), but not two
+ * calls concurrently.
  */
 size_t pb_workspace_bytes(int64_t batch, int64_t cols, int32_t act_bits);
 
@@ -216,6 +219,33 @@ pb_status pb_lstm_step(const float* x_t, const float* h, const float* c,
                        const float* b_ih, const float* b_hh, int32_t k_used_ih,
                        int32_t k_used_hh, int32_t act_bits, int64_t batch,
                        float* h_out, float* c_out, void* ws, size_t ws_bytes, pb_stream s);
+
+/* LSTM over a sequence (P:258-260 LSTM LM, P:317 NLI encoders;
+ * reading G15).  Rows of W_ih [4H][E], W_hh [4H][H] and bias [4H] are
+ * GATE-INTERLEAVED: row 4k + q is gate q (i, f, g, o) of hidden unit k, i.e.
+ * PyTorch's gate-major rows permuted (paper_2003_00822_b200.interleave_gates);
+ * Q(W) is permutation-invariant, so the codes are those of the gate-major
+ * matrix.  Steps:
+ *   1. gx[t][b] = W_ih x[t][b] + bias for all steps*batch columns in one
+ *      batched call (the input projection hoisted out of the recurrence);
+ *   2. per t: pre = W_hh h_t + gx[t]; c_{t+1} = sigmoid(f) c_t + sigmoid(i) tanh(g),
+ *      h_{t+1} = sigmoid(o) tanh(c_{t+1}) -- ONE fused tensor-engine launch
+ *      (a1-a5 + the cell in the finalisation, which holds the 4 gate rows of
+ *      a unit in adjacent lanes), else planes + GEMM + a cell kernel.
+ *   x      device [steps][batch][E];  h0, c0 device [batch][H];
+ *   bias   device [4H] (b_ih + b_hh, interleaved) or NULL;
+ *   h_seq  device [steps][batch][H]: h_1 .. h_steps (required);
+ *   c_seq  device [steps][batch][H] or NULL: c_1 .. c_steps;
+ *   c_last device [batch][H]: c_steps (required).
+ * Stream-ordered, graph-capturable, no allocation.  PB_EINVAL: shapes, NULLs,
+ * workspace < pb_lstm_seq_workspace_bytes. */
+size_t pb_lstm_seq_workspace_bytes(int64_t steps, int64_t batch, int64_t in_cols,
+                                   int64_t hidden, int32_t act_bits);
+pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float* h0,
+                      const float* c0, const pb_weights* w_ih, const pb_weights* w_hh,
+                      const float* bias, int32_t k_used_ih, int32_t k_used_hh,
+                      int32_t act_bits, float* h_seq, float* c_seq, float* c_last,
+                      void* ws, size_t ws_bytes, pb_stream s);
 
 /* Select the binary-product engine (process-wide; default AUTO). */
 pb_status pb_set_engine(int32_t engine);

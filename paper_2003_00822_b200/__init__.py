@@ -59,6 +59,8 @@ _SIGS = {
     "pb_cell_workspace_bytes": ([_i64, _i64, _i64, _i32, _i32], _sz),
     "pb_rnn_step": ([_p, _p, _W, _W, _p, _p, _i32, _i32, _i32, _i64, _p, _p, _sz, _p], _i32),
     "pb_lstm_step": ([_p, _p, _p, _W, _W, _p, _p, _i32, _i32, _i32, _i64, _p, _p, _p, _sz, _p], _i32),
+    "pb_lstm_seq_workspace_bytes": ([_i64, _i64, _i64, _i64, _i32], _sz),
+    "pb_lstm_seq": ([_p, _i64, _i64, _p, _p, _W, _W, _p, _i32, _i32, _i32, _p, _p, _p, _p, _sz, _p], _i32),
     "pb_set_engine": ([_i32], _i32),
     "pb_get_engine": ([], _i32),
     "pb_shard_rows": ([_i64, _i32, _i32, C.POINTER(_i64), C.POINTER(_i64)], _i32),
@@ -260,6 +262,41 @@ def lstm_step(x, h, c, w_ih, w_hh, b_ih=None, b_hh=None, k_used_ih=None, k_used_
                        _ptr(b_hh), k_used_ih or w_ih.layers, k_used_hh or w_hh.layers, act_bits, B,
                        _ptr(h_out), _ptr(c_out), ws.ptr, ws.nbytes, _stream(stream)))
     return h_out, c_out
+
+
+def interleave_gates(a, gates=4):
+    """Gate-major rows (PyTorch nn.LSTM: [i; f; g; o], each H rows) -> gate-interleaved rows
+    (row 4k + q = gate q of unit k), the layout pb_lstm_seq reads (numpy, host; any trailing
+    shape, e.g. W [4H][E] or a bias [4H])."""
+    a = np.asarray(a)
+    H = a.shape[0] // gates
+    return np.ascontiguousarray(a.reshape((gates, H) + a.shape[1:]).swapaxes(0, 1).reshape(a.shape))
+
+
+def deinterleave_gates(a, gates=4):
+    """Inverse of interleave_gates."""
+    a = np.asarray(a)
+    H = a.shape[0] // gates
+    return np.ascontiguousarray(a.reshape((H, gates) + a.shape[1:]).swapaxes(0, 1).reshape(a.shape))
+
+
+def lstm_seq(x, h0, c0, w_ih, w_hh, bias=None, k_used_ih=None, k_used_hh=None, act_bits=16, h_seq=None,
+             c_seq=None, c_last=None, ws=None, stream=None):
+    """pb_lstm_seq: x [T][B][E], h0/c0 [B][H] (device float32); w_ih, w_hh, bias with
+    gate-interleaved rows (interleave_gates).  Returns (h_seq [T][B][H], c_last [B][H])."""
+    import torch
+    T, B, E = x.shape
+    H = h0.shape[1]
+    if h_seq is None:
+        h_seq = torch.empty((T, B, H), dtype=torch.float32, device=x.device)
+    if c_last is None:
+        c_last = torch.empty((B, H), dtype=torch.float32, device=x.device)
+    if ws is None:
+        ws = Workspace(pb_lstm_seq_workspace_bytes(T, B, E, H, act_bits), x.device)
+    check(pb_lstm_seq(_ptr(x), T, B, _ptr(h0), _ptr(c0), C.byref(w_ih.desc), C.byref(w_hh.desc), _ptr(bias),
+                      k_used_ih or w_ih.layers, k_used_hh or w_hh.layers, act_bits, _ptr(h_seq), _ptr(c_seq),
+                      _ptr(c_last), ws.ptr, ws.nbytes, _stream(stream)))
+    return h_seq, c_last
 
 
 def shard_rows(rows_total, nranks, rank):

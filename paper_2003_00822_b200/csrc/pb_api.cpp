@@ -436,9 +436,17 @@ static pb_status validate_gemm(const void* ws, size_t ws_bytes, int64_t batch, c
 // Steps a3-a5 (and, when x is given and the tensor engine takes the shape, a1-a2
 // fused into the same kernel).  Returns PB_EINVAL with *fused_done = false when x
 // is given but the fused path does not apply (the caller then runs a1-a2 first).
+// Fused LSTM cell operands of one pb_lstm_seq step (GemmArgs cell mode), or null.
+struct CellOut {
+    int64_t H;
+    const float* c;     // [B][H]
+    float* h_out;       // [B][H]
+    float* c_out;       // [B][H]
+};
+
 static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
                           float* y, int64_t* acc, const float* bias, int32_t fn, int32_t accumulate, pb_stream s,
-                          const float* x, int32_t act_frac, bool* fused_done) {
+                          const float* x, int32_t act_frac, bool* fused_done, const CellOut* cell = nullptr) {
     if (fused_done) *fused_done = false;
 
     const pb::WsLayout l = pb::ws_layout(batch, w->kwords, act_bits);
@@ -473,6 +481,11 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     g.gbar = g.counters + pb::kMaxTiles;
     g.work = g.counters + pb::kMaxTiles + 2;
     g.ebar = g.counters + pb::kMaxTiles + 4;
+    g.cell = 0;
+    g.H = 0;
+    g.cell_c = nullptr;
+    g.cell_h = nullptr;
+    g.cell_c_out = nullptr;
 
     cudaError_t e;
     const cudaStream_t cs = static_cast<cudaStream_t>(s);
@@ -495,12 +508,20 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
             gs.acc = acc ? reinterpret_cast<long long*>(acc) + b0 * w->rows : nullptr;
             gs.f = g.f + b0;
             gs.xsum = g.xsum + b0 * pb::kXsumStride;
+            if (cell) {
+                gs.cell = 1;
+                gs.H = cell->H;
+                gs.cell_c = cell->c + b0 * cell->H;
+                gs.cell_h = cell->h_out + b0 * cell->H;
+                gs.cell_c_out = cell->c_out + b0 * cell->H;
+            }
             e = pb::launch_gemm_tc(gs, cs);
             if (e != cudaSuccess) return cuda_fail(e, "fused bitgemm launch");
         }
         *fused_done = true;
         return PB_OK;
     }
+    if (cell) return PB_EINVAL;                  // the cell is fused on the tensor engine's fused path only
     if (g_engine == PB_ENGINE_MMA) {
         if (!pb::tc_supported(g))
             return fail(PB_EINVAL, "PB_ENGINE_MMA on the split path needs act_bits*batch <= 64, batch <= 32 "
@@ -608,6 +629,76 @@ pb_status pb_lstm_step(const float* x_t, const float* h, const float* c, const p
     if (!h_out || !c_out || !c) return fail(PB_EINVAL, "c/h_out/c_out is NULL");
     cudaError_t e = pb::launch_lstm_cell(gates, c, batch, w_hh->cols, h_out, c_out, static_cast<cudaStream_t>(s));
     if (e != cudaSuccess) return cuda_fail(e, "lstm_cell launch");
+    return PB_OK;
+}
+
+// ------------------------------------------------------------ LSTM sequence
+size_t pb_lstm_seq_workspace_bytes(int64_t steps, int64_t batch, int64_t in_cols, int64_t hidden, int32_t act_bits) {
+    if (steps < 0 || batch < 0 || in_cols < 0 || hidden < 0) return 0;
+    const int64_t k = in_cols > hidden ? in_cols : hidden;
+    const int64_t cols = steps * batch > batch ? steps * batch : batch;
+    return pb::align_up(pb_workspace_bytes(cols, k, act_bits)) +
+           pb::align_up(sizeof(float) * (size_t)cols * 4 * (size_t)hidden) +
+           2 * pb::align_up(sizeof(float) * (size_t)batch * (size_t)hidden);
+}
+
+pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float* h0, const float* c0,
+                      const pb_weights* w_ih, const pb_weights* w_hh, const float* bias, int32_t k_used_ih,
+                      int32_t k_used_hh, int32_t act_bits, float* h_seq, float* c_seq, float* c_last, void* ws,
+                      size_t ws_bytes, pb_stream s) {
+    g_err[0] = 0;
+    pb_status st;
+    if ((st = check_weights(w_ih)) != PB_OK) return st;
+    if ((st = check_weights(w_hh)) != PB_OK) return st;
+    const int64_t H = w_hh->cols, E = w_ih->cols;
+    if (w_ih->rows != 4 * H || w_hh->rows != 4 * H)
+        return fail(PB_EINVAL, "W_ih/W_hh must have 4*H rows (H = W_hh cols = %lld)", (long long)H);
+    if (steps < 0 || batch < 0) return fail(PB_EINVAL, "steps/batch < 0");
+    if (steps == 0 || batch == 0 || H == 0) return PB_OK;
+    if (!x || !h0 || !c0 || !h_seq || !c_last) return fail(PB_EINVAL, "x/h0/c0/h_seq/c_last is NULL");
+    const size_t need = pb_lstm_seq_workspace_bytes(steps, batch, E, H, act_bits);
+    if (!ws || !aligned(ws, 16) || ws_bytes < need) return fail(PB_EINVAL, "lstm_seq workspace %zu < %zu", ws_bytes, need);
+    const int64_t k = E > H ? E : H;
+    const int64_t cols = steps * batch;
+    const size_t act_ws = pb::align_up(pb_workspace_bytes(cols, k, act_bits));
+    char* base = static_cast<char*>(ws);
+    float* gx = reinterpret_cast<float*>(base + act_ws);
+    float* cb[2];
+    cb[0] = reinterpret_cast<float*>(base + act_ws + pb::align_up(sizeof(float) * (size_t)cols * 4 * (size_t)H));
+    cb[1] = cb[0] + pb::align_up(sizeof(float) * (size_t)batch * (size_t)H) / sizeof(float);
+    // 1. the input projection of every timestep in one batched call (GEMM regime):
+    //    gx[t][b] = W_ih x[t][b] + bias (gate-interleaved rows)
+    if ((st = act_and_gemm(x, cols, w_ih, k_used_ih, act_bits, PB_ACT_AUTO, bias, PB_FN_NONE, gx, nullptr, ws,
+                           act_ws, s)) != PB_OK)
+        return st;
+    // 2. per timestep: W_hh h_t + gx[t], then the cell -- fused into the tensor engine's
+    //    finalisation when the shape allows, else split (planes + GEMM + cell kernel)
+    for (int64_t t = 0; t < steps; ++t) {
+        const float* h_in = t == 0 ? h0 : h_seq + (t - 1) * batch * H;
+        const float* c_in = t == 0 ? c0 : (c_seq ? c_seq + (t - 1) * batch * H : cb[(t - 1) & 1]);
+        float* h_out = h_seq + t * batch * H;
+        float* c_out = c_seq ? c_seq + t * batch * H : (t == steps - 1 ? c_last : cb[t & 1]);
+        float* gt = gx + t * batch * 4 * H;
+        const CellOut co{H, c_in, h_out, c_out};
+        bool fused = false;
+        st = run_gemm(ws, batch, w_hh, k_used_hh, act_bits, gt, nullptr, nullptr, PB_FN_NONE, 1, s, h_in,
+                      PB_ACT_AUTO, &fused, &co);
+        if (st != PB_OK && st != PB_EINVAL) return st;
+        if (!fused) {
+            g_err[0] = 0;
+            if ((st = pb_act_quantize(h_in, batch, H, act_bits, PB_ACT_AUTO, ws, act_ws, s)) != PB_OK) return st;
+            if ((st = run_gemm(ws, batch, w_hh, k_used_hh, act_bits, gt, nullptr, nullptr, PB_FN_NONE, 1, s, nullptr,
+                               0, nullptr)) != PB_OK)
+                return st;
+            cudaError_t e = pb::launch_lstm_cell_ilv(gt, c_in, batch, H, h_out, c_out, static_cast<cudaStream_t>(s));
+            if (e != cudaSuccess) return cuda_fail(e, "lstm_cell_ilv launch");
+        }
+        if (c_seq && t == steps - 1) {
+            cudaError_t e = cudaMemcpyAsync(c_last, c_out, sizeof(float) * (size_t)batch * (size_t)H,
+                                            cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(s));
+            if (e != cudaSuccess) return cuda_fail(e, "c_last copy");
+        }
+    }
     return PB_OK;
 }
 

@@ -12,7 +12,7 @@
 namespace pb {
 namespace {
 
-__device__ __forceinline__ float sigm(float v) { return 1.f / (1.f + expf(-v)); }
+__device__ __forceinline__ float sigm(float v) { return sigmoidf_(v); }
 
 __global__ void lstm_cell_kernel(const float* __restrict__ gates, const float* __restrict__ c,
                                  int64_t B, int64_t H, float* __restrict__ h_out,
@@ -24,13 +24,27 @@ __global__ void lstm_cell_kernel(const float* __restrict__ gates, const float* _
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = t / H, k = t - b * H;
         const float* g = gates + b * 4 * H;
-        const float ig = sigm(g[k]);
-        const float fg = sigm(g[H + k]);
-        const float gg = tanhf(g[2 * H + k]);
-        const float og = sigm(g[3 * H + k]);
-        const float cn = fg * c[t] + ig * gg;
+        float hn, cn;
+        lstm_cell(g[k], g[H + k], g[2 * H + k], g[3 * H + k], c[t], hn, cn);
         c_out[t] = cn;
-        h_out[t] = og * tanhf(cn);
+        h_out[t] = hn;
+    }
+}
+
+// Gate-interleaved pre-activations (pb_lstm_seq: row 4k + gate), [B][H][4].
+__global__ void lstm_cell_ilv_kernel(const float* __restrict__ gates, const float* __restrict__ c,
+                                     int64_t B, int64_t H, float* __restrict__ h_out,
+                                     float* __restrict__ c_out)
+{
+    pdl_wait();
+    const int64_t n = B * H;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const float4 g = reinterpret_cast<const float4*>(gates)[t];
+        float hn, cn;
+        lstm_cell(g.x, g.y, g.z, g.w, c[t], hn, cn);
+        c_out[t] = cn;
+        h_out[t] = hn;
     }
 }
 
@@ -78,6 +92,22 @@ cudaError_t launch_lstm_cell(const float* gates, const float* c, int64_t B, int6
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, lstm_cell_kernel, gates, c, B, H, h_out, c_out);
+}
+
+cudaError_t launch_lstm_cell_ilv(const float* gates, const float* c, int64_t B, int64_t H,
+                                 float* h_out, float* c_out, cudaStream_t s)
+{
+    if (B * H == 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid_for(B * H, 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, lstm_cell_ilv_kernel, gates, c, B, H, h_out, c_out);
 }
 
 cudaError_t launch_rnn_cell(const float* gates, int64_t B, int64_t H, float* h_out, cudaStream_t s)

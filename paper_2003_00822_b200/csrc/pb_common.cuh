@@ -145,6 +145,16 @@ __device__ __forceinline__ float dequant(long long acc, double scale, int f) {
     t = ldexp(t, -f);
     return __double2float_rn(t);
 }
+// LSTM cell (reading G15: PyTorch nn.LSTM gates i, f, g, o; fp32 as P:128 keeps the
+// nonlinearities in full precision): c' = sigmoid(f) c + sigmoid(i) tanh(g),
+// h' = sigmoid(o) tanh(c').
+__device__ __forceinline__ float sigmoidf_(float v) { return 1.f / (1.f + expf(-v)); }
+__device__ __forceinline__ void lstm_cell(float gi, float gf, float gg, float go, float c, float& h_out,
+                                          float& c_out) {
+    const float cn = sigmoidf_(gf) * c + sigmoidf_(gi) * tanhf(gg);
+    c_out = cn;
+    h_out = sigmoidf_(go) * tanhf(cn);
+}
 __device__ __forceinline__ float apply_fn(float v, int fn) {
     switch (fn) {
         case 1: return v > 0.f ? v : 0.f;

@@ -932,7 +932,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             for (int pp = 0; pp < g.nsplit; ++pp) sx += (unsigned long long)xs[pp];
             return sx;
         };
-        auto finish = [&](int b, int64_t row, unsigned long long t) {
+        // a5: y = dequant(acc) (+ bias, + y when accumulating), then fn -- or, in cell mode
+        // (pb_lstm_seq), the LSTM cell over the 4 gate rows of a hidden unit (lanes 4j..4j+3)
+        auto preact = [&](int b, int64_t row, unsigned long long t) -> float {
             t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
             const long long accv = (long long)t;
             const int64_t o = (int64_t)b * g.R + row;
@@ -940,7 +942,24 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             float yv = dequant(accv, g.scale, g.x ? bars.f[b] : g.f[b]);
             if (g.bias) yv += g.bias[row];
             if (g.accumulate) yv += g.y[o];
-            g.y[o] = apply_fn(yv, g.fn);
+            return yv;
+        };
+        auto finish_tile_row = [&](int b, int64_t row, unsigned long long t) {   // warp-uniform call
+            if (!g.cell) {
+                if (row < g.R) g.y[(int64_t)b * g.R + row] = apply_fn(preact(b, row, t), g.fn);
+                return;
+            }
+            const float v = row < g.R ? preact(b, row, t) : 0.f;
+            const int q0 = lane & ~3;
+            const float gi = __shfl_sync(0xffffffffu, v, q0), gf = __shfl_sync(0xffffffffu, v, q0 + 1);
+            const float gg = __shfl_sync(0xffffffffu, v, q0 + 2), go = __shfl_sync(0xffffffffu, v, q0 + 3);
+            if ((lane & 3) == 0 && row < g.R) {
+                const int64_t i = (int64_t)b * g.H + (row >> 2);
+                float hn, cn;
+                lstm_cell(gi, gf, gg, go, g.cell_c[i], hn, cn);
+                g.cell_h[i] = hn;
+                g.cell_c_out[i] = cn;
+            }
         };
         if (g.x)
             fused_prologue<NPAD>(g, p, bars, threadIdx.x - kEpi0 * 32, btile0,
@@ -1057,7 +1076,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             for (int b = 0; b < g.B; ++b) {
                 const unsigned long long t = __ldcg(ab + b * kTcRows);
                 ab[b * kTcRows] = 0;                  // every call leaves the accumulators zero
-                if (row < g.R) finish(b, row, t);
+                finish_tile_row(b, row, t);
             }
         }
         if (TLP(g) && ew == 0 && lane == 0) bars.t_cend = gtimer();

@@ -62,7 +62,14 @@ inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     l.npad = tc_npad(bs, act_bits);
     l.off_count = 0;
     l.off_slots = align_up(sizeof(int32_t) * (kMaxTiles + 6));
-    const size_t slots = l.npad ? sizeof(long long) * kAccTiles * (size_t)bs * kTcRows : 0;
+    // partial-tile sums sized for the largest slice this act_bits can launch (not this batch's),
+    // so calls of different batch sizes with the same act_bits can share one workspace: the
+    // region every call expects zero on entry is the same for all of them
+    int64_t bs_max = act_bits > 0 ? kTcMaxN / act_bits : 1;
+    if (bs_max > kTcMaxB) bs_max = kTcMaxB;
+    if (bs_max < 1) bs_max = 1;
+    if (bs_max < bs) bs_max = bs;
+    const size_t slots = l.npad ? sizeof(long long) * kAccTiles * (size_t)bs_max * kTcRows : 0;
     l.off_f = align_up(l.off_slots + slots);
     l.off_xsum = align_up(l.off_f + sizeof(int32_t) * (size_t)batch);
     l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kXsumStride);
@@ -107,6 +114,14 @@ struct GemmArgs {
     int* gbar;                    // grid barrier {arrival count, generation}
     int* work;                    // tensor engine {item claim counter, finished CTAs}, zero between calls
     int* ebar;                    // tensor engine end-of-work grid barrier {arrival count, generation}
+    // fused LSTM cell (pb_lstm_seq, tensor engine): rows are gate-interleaved (row 4k + gate,
+    // gates i, f, g, o); the finalisation applies the cell to the four pre-activations of
+    // hidden unit k (dequant + bias + y when accumulate) and writes h, c instead of y
+    int cell;                     // 0 = none, 1 = LSTM
+    int64_t H;                    // hidden units (R / 4)
+    const float* cell_c;          // [B][H] c_t
+    float* cell_h;                // [B][H] h_{t+1}
+    float* cell_c_out;            // [B][H] c_{t+1}
 };
 
 // Diagnostics timeline (PB_TC_DEBUG=6): device log, [0] = record counter,
@@ -122,6 +137,8 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, cudaStream_t s);
 bool tc_supported(const GemmArgs& g);
 cudaError_t launch_lstm_cell(const float* gates, const float* c, int64_t B, int64_t H,
                              float* h_out, float* c_out, cudaStream_t s);
+cudaError_t launch_lstm_cell_ilv(const float* gates, const float* c, int64_t B, int64_t H,
+                                 float* h_out, float* c_out, cudaStream_t s);
 cudaError_t launch_rnn_cell(const float* gates, int64_t B, int64_t H, float* h_out,
                             cudaStream_t s);
 cudaError_t launch_permute_shards(const float* gathered, int64_t B, int64_t rows_per_rank,
