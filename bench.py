@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="oracle cpu_baseline budget")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline (profiling runs)")
     p.add_argument("--no-compare", action="store_true", help="skip the cuBLAS fp32/bf16/int8 comparison (f3)")
+    p.add_argument("--no-lstm", action="store_true", help="skip the LSTM-LM (configs[2]) sequence timing (f1)")
     p.add_argument("--ref-budget", type=float, default=120.0, help="--impl reference total budget (s)")
     return p.parse_args()
 
@@ -503,6 +504,57 @@ def main():
             except Exception as e:      # comparison only: report, never fail the bench
                 compare["systems"][name] = {"error": str(e)[:200]}
 
+    # ---- LSTM LM (BASELINE configs[2]: H = 2048, 4-gate matvecs per timestep; E = H, reading
+    #      G15): pb_lstm_seq over T timesteps (hoisted input projection + one fused launch per
+    #      step with the cell in the epilogue) vs T pb_lstm_step calls, both CUDA graphs
+    lstm = None
+    if not args.no_lstm and N == 1:
+        try:
+            Hh, Tt = 2048, 32
+            lstm = {"config": f"LSTM LM H={Hh}, E={Hh}, T={Tt} timesteps, a=16; W_hh per step stays L2-resident "
+                              "(recurrence: the same 4H x H weights every step)", "points": []}
+            rng = np.random.default_rng(synth.seed(3, 0))
+            Wih = (rng.standard_normal((4 * Hh, Hh)) / math.sqrt(Hh)).astype(np.float32)
+            Whh = (rng.standard_normal((4 * Hh, Hh)) / math.sqrt(Hh)).astype(np.float32)
+            bb = (0.1 * rng.standard_normal(4 * Hh)).astype(np.float32)
+            for Lx, Bx in ((2, 1), (4, 1), (8, 1), (16, 1), (4, 4), (4, 16)):
+                wi = pb.PackedWeights.quantize(pb.interleave_gates(Wih), Lx)
+                wh = pb.PackedWeights.quantize(pb.interleave_gates(Whh), Lx)
+                wig, whg = pb.PackedWeights.quantize(Wih, Lx), pb.PackedWeights.quantize(Whh, Lx)
+                xs_ = torch.randn(Tt, Bx, Hh, device="cuda")
+                h0 = torch.tanh(torch.randn(Bx, Hh, device="cuda"))
+                c0 = torch.randn(Bx, Hh, device="cuda")
+                bi = torch.from_numpy(pb.interleave_gates(bb)).cuda()
+                bg = torch.from_numpy(bb).cuda()
+                zb = torch.zeros_like(bg)
+                wsl = pb.Workspace(pb.pb_lstm_seq_workspace_bytes(Tt, Bx, Hh, Hh, a))
+                hs = torch.empty(Tt, Bx, Hh, device="cuda")
+                cl = torch.empty(Bx, Hh, device="cuda")
+                wsc = pb.Workspace(pb.pb_cell_workspace_bytes(Bx, Hh, Hh, a, 4))
+                hb = [torch.empty(Bx, Hh, device="cuda") for _ in range(2)]
+                cb_ = [torch.empty(Bx, Hh, device="cuda") for _ in range(2)]
+
+                def seq_fn(_w, s_):
+                    pb.lstm_seq(xs_, h0, c0, wi, wh, bi, act_bits=a, h_seq=hs, c_last=cl, ws=wsl, stream=s_)
+
+                def step_fn(_w, s_):
+                    h, c = h0, c0
+                    for t in range(Tt):
+                        pb.lstm_step(xs_[t], h, c, wig, whg, bg, zb, act_bits=a, h_out=hb[t & 1],
+                                     c_out=cb_[t & 1], ws=wsc, stream=s_)
+                        h, c = hb[t & 1], cb_[t & 1]
+                pt_ = {"L": Lx, "batch": Bx}
+                for nm, fn_ in (("lstm_seq", seq_fn), ("lstm_step_loop", step_fn)):
+                    gp = capture([None], fn_, 4)
+                    tt = time_graphs(gp, 4, 2) / 4
+                    pt_[nm + "_us_per_timestep"] = tt * 1e3 / Tt
+                    del gp
+                lstm["points"].append(pt_)
+                del wi, wh, wig, whg, wsl, wsc
+                torch.cuda.empty_cache()
+        except Exception as e:          # extra workload: report, never fail the bench
+            lstm = {"error": str(e)[:300]}
+
     # ---- CPU oracle baseline (rank 0, N = 1 only), bounded sample
     cpu = None
     if rank == 0 and N == 1 and not args.no_cpu:
@@ -532,7 +584,7 @@ def main():
                                  f"{M * w0.nbytes() / 2**20:.0f} MiB >= 2x L2 ({l2 / 2**20:.0f} MiB)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": (launches_per_call + (1 if (N > 1 and B > 1) else 0)) * args.steps,
-                "clocks": clocks, "per_L": per_L, "per_kused": per_k, "compare": compare,
+                "clocks": clocks, "per_L": per_L, "per_kused": per_k, "compare": compare, "lstm_lm": lstm,
                 "context": "paper: >8x end-to-end vs FP32 on a Tesla T4 (P:28, P:216) -- context, not target"}
         print(json.dumps(line), flush=True)
     if N > 1:

@@ -493,13 +493,20 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
         // fused a1-a5, one launch per batch slice of <= 64 plane columns (pb::tc_slice); every
         // slice must fit the tensor engine, else the caller runs the split path
         if (g_engine == PB_ENGINE_POPC) return PB_EINVAL;
-        const int64_t bs = pb::tc_slice(batch, act_bits);
+        // the widest slice whose launches all fit the engine (more accumulator groups leave
+        // fewer TMEM columns for the A ring, so a wide N may need a narrower slice)
         pb::GemmArgs gs = g;
-        for (int64_t b0 = 0; b0 < batch; b0 += bs) {
-            gs.B = batch - b0 < bs ? batch - b0 : bs;
-            gs.npad = pb::tc_npad(gs.B, act_bits);
-            if (!pb::tc_supported(gs)) return PB_EINVAL;
-        }
+        auto slices_fit = [&](int64_t bs) {
+            for (int64_t b0 = 0; b0 < batch; b0 += bs) {
+                gs.B = batch - b0 < bs ? batch - b0 : bs;
+                gs.npad = pb::tc_npad(gs.B, act_bits);
+                if (!pb::tc_supported(gs)) return false;
+            }
+            return true;
+        };
+        int64_t bs = pb::tc_slice(batch, act_bits);
+        while (bs > 1 && !slices_fit(bs)) bs = (bs + 1) / 2;
+        if (!slices_fit(bs)) return PB_EINVAL;
         for (int64_t b0 = 0; b0 < batch; b0 += bs) {
             gs.B = batch - b0 < bs ? batch - b0 : bs;
             gs.npad = pb::tc_npad(gs.B, act_bits);

@@ -32,6 +32,7 @@ def torch():
     (3, 8, 160, 128, 4, 4, "auto"),      # 2 batch slices per step, ragged H tile
     (2, 2, 64, 96, 1, 1, "auto"),        # binary weights (L = 1)
     (3, 2, 128, 96, 4, 4, "popc"),       # split path: planes + POPC GEMM + interleaved cell kernel
+    (3, 2, 128, 2048, 16, 16, "auto"),   # hoisted W_ih with 2 accumulator groups (narrowed slices)
 ])
 def test_lstm_seq(pb, torch, orc, T, B, H, E, L_ih, L_hh, engine):
     s = synth.seed(7, T + 10 * B + H + E)

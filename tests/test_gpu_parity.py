@@ -72,6 +72,7 @@ CASES = [  # R, K, B, L, k_used, a
     (257, 1030, 3, 5, 4, 16),     # N = 48 -> padded to 64
     (129, 3000, 8, 8, 7, 8),      # N = 64, a = 8
     (200, 1500, 37, 4, 4, 16),    # 10 slices of <= 4 columns, ragged last slice
+    (512, 2048, 8, 16, 16, 16),   # 2 accumulator groups: N = 64 slices narrowed to N = 32
 ]
 
 
