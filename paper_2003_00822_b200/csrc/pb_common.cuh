@@ -118,6 +118,16 @@ __device__ __forceinline__ void put_b_operand(uint8_t* bexp, int npad, int64_t w
                    ((p >> 3) & 0x11111111u) << 2);
 }
 
+// The same B operand word into a shared-memory tile (explicit st.shared: a generic store
+// would resolve its address space at run time).
+__device__ __forceinline__ void put_b_operand_smem(uint32_t tile_s, int npad, int64_t w, int n, uint32_t p) {
+    const uint32_t a = tile_s + (uint32_t)((w >> 1) * npad * 32 + (w & 1) * 128 + (n >> 3) * 256 + (n & 7) * 16);
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"((p & 0x11111111u) << 2),
+                 "r"(((p >> 1) & 0x11111111u) << 2), "r"(((p >> 2) & 0x11111111u) << 2),
+                 "r"(((p >> 3) & 0x11111111u) << 2)
+                 : "memory");
+}
+
 // Next diagnostics-timeline record (pb_internal.h, pb_debug_timeline) or null when full.
 __device__ __forceinline__ long long* tl_record(long long* tl) {
     const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(tl), 1ull);

@@ -383,7 +383,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     constexpr int kPT = 32 * kPW;
     constexpr int kCx = 8;                             // first-chunk values prefetched per thread
     const int pw = pt >> 5, lane = pt & 31;
-    long long tpw = 0, tmax = 0, tc0 = 0, ttr = 0, tfb = 0, tcg = 0;
+    long long tpw = 0, tmax = 0, tc0 = 0, ttr = 0, tfb = 0, tcg = 0, cyc_ballot = 0, cyc_put = 0;
     pdl_wait();                                        // x may be the previous kernel's output
     if TLP(g) tpw = gtimer();
     const int B = (int)g.B;
@@ -495,11 +495,12 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     if (et == 0) mbar_arrive(&bars.slice_done);
     // ---- a1 (part 2) + a2 for the first chunk: cast, ballot-transpose (x_q fits 32 bits:
     // a <= 32), e2m1 B rows straight into B stage 0
+    const uint32_t bstage0_s = smem_u32(bstage0);
     auto put0 = [&](int it, uint32_t mine) {
         const int b = it / kChunkWords, wl = it - b * kChunkWords;
-        if (lane < g.a) put_b_operand(bstage0, NPAD, wl, b * g.a + lane, mine);
+        if (lane < g.a) put_b_operand_smem(bstage0_s, NPAD, wl, b * g.a + lane, mine);
         if (b == B - 1)
-            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand(bstage0, NPAD, wl, n, 0u);
+            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand_smem(bstage0_s, NPAD, wl, n, 0u);
     };
     // kCx items (itb + kPW * k) per step: kCx independent ballot chains in flight
     auto chunk_group = [&](int itb, const float (&v)[kCx]) {
@@ -510,6 +511,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
             u[k] = (uint32_t)act_cast(v[k], bars.f[it < nci ? it / kChunkWords : 0], g.a);
             mm[k] = 0;
         }
+        const long long c1 = kTimeline ? clock64() : 0;
 #pragma unroll 1
         for (int j = 0; j < g.a; ++j) {
             const uint32_t bit = 1u << (g.a - 1 - j);
@@ -519,9 +521,14 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
                 if (lane == j) mm[k] = w;
             }
         }
+        const long long c2 = kTimeline ? clock64() : 0;
 #pragma unroll
         for (int k = 0; k < kCx; ++k)
             if (itb + kPW * k < nci) put0(itb + kPW * k, mm[k]);
+        if (kTimeline) {
+            cyc_ballot += c2 - c1;
+            cyc_put += clock64() - c2;
+        }
     };
     chunk_group(pw, cx);                               // warp-uniform bounds (ballots inside)
 #pragma unroll 1
@@ -542,7 +549,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     if (TLP(g) && et == 0) {
         long long* r = tl_record(TLP(g));
         if (r) {
-            const long long rec[10] = {2, blockIdx.x, 0, 0, tpw, tmax, tc0, ttr, tfb, tcg};
+            const long long rec[10] = {2, blockIdx.x, cyc_ballot, cyc_put, tpw, tmax, tc0, ttr, tfb, tcg};
             for (int q = 0; q < 10; ++q) r[q] = rec[q];
         }
     }

@@ -40,7 +40,8 @@ if len(pr):
               f"slice done {f(q[:,7]).min():8.2f}..{f(q[:,7]).max():8.2f}")
         if q[:, 8].any():
             print(f"   max->f_b med {np.median(q[:,8]-q[:,5])/1e3:.2f}  f_b->groups done med {np.median(q[:,9]-q[:,8])/1e3:.2f}"
-                  f"  groups->chunk0 published med {np.median(q[:,6]-q[:,9])/1e3:.2f} us")
+                  f"  groups->chunk0 published med {np.median(q[:,6]-q[:,9])/1e3:.2f} us; chunk groups: ballot loop "
+                  f"med {np.median(q[:,2]):.0f} cycles, stores med {np.median(q[:,3]):.0f} cycles")
 ep = rec[rec[:, 0] == 3]
 if len(ep):
     # per epilogue segment: d_full wake -> TMEM drained -> slot/atomic done -> y stored
