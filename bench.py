@@ -234,11 +234,13 @@ def main():
         dist.all_reduce(mn, dist.ReduceOp.MIN)
         dist.all_reduce(mx, dist.ReduceOp.MAX)
 
+    Wl_dev = torch.from_numpy(Wl).cuda()     # offline packing on the GPU (same bytes as the host packer)
+
     def pack(Lx):
         if Lx == 1:
             assert N == 1, "binary sweep point is single-GPU"
             return pb.PackedWeights.quantize(Wl, 1, pb.PB_Q_BINARY)
-        return pb.PackedWeights.quantize_step(Wl, Lx, pb.shard_grid_step(mn.item(), mx.item(), Lx))
+        return pb.PackedWeights.quantize_device(Wl_dev, Lx, step=pb.shard_grid_step(mn.item(), mx.item(), Lx))
 
     def rotation(w):
         nb = w.nbytes()

@@ -124,6 +124,22 @@ pb_status pb_quantize_pack_weights_step(const float* W_host, int64_t rows, int64
                                         int32_t layers, double step, void* dst,
                                         int32_t dst_is_device, pb_stream s, pb_weights* out);
 
+/* Step a0 on the GPU, for a float32 W [rows][cols] already
+ * in device memory: the PB_Q_GRID quantiser (readings G4, G5) and
+ * the bitlayer packer, producing exactly the bytes and scale of
+ * pb_quantize_pack_weights(PB_Q_GRID) / _step.  step == 0: grid from the
+ * extrema (clip > 0 clips first; ws = pb_pack_device_workspace_bytes() of
+ * device scratch for the min/max partials); step > 0: that grid step (row
+ * shards, as pb_quantize_pack_weights_step; clip and ws unused).
+ * dst: device, pb_packed_bytes(rows, cols, layers), 16-byte aligned.  Offline:
+ * synchronises the stream.  PB_EINVAL for layers outside [2,16] (binary and
+ * literal Alg. 1 packing stay on the host), PB_EDEGENERATE as the host packer. */
+size_t pb_pack_device_workspace_bytes(void);
+pb_status pb_quantize_pack_weights_device(const float* W_dev, int64_t rows, int64_t cols,
+                                          int32_t layers, float clip, double step, void* dst,
+                                          void* ws, size_t ws_bytes, pb_stream s,
+                                          pb_weights* out);
+
 /* Pack caller-supplied integer codes [rows][cols] (L-bit two's complement;
  * for offset = 1, L must be 1 and codes are +-1 meaning 1 - 2*bit).  Used by
  * tests and by callers with their own quantiser.  PB_ERANGE if a code does
@@ -140,11 +156,10 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
 /*
  * Workspace of one call (batch columns of a layer with `cols` inputs):
  *   [stream-K tile counters int32 x 8192]     zero on entry, left zero on exit
- *   [grid barrier int32 x 2]                  arrival count (zero on entry,
- *                                             left zero) + generation
+ *   [grid barrier uint64]                     monotonic arrival counter (any
+ *                                             value on entry; grows by 2^20 per call)
  *   [work counters int32 x 2]                 zero on entry, left zero
- *   [end barrier int32 x 2]                   arrival count (zero on entry,
- *                                             left zero) + generation
+ *   [end barrier uint64]                      monotonic arrival counter
  *   [tensor-engine partial-tile sums int64 x 2048 x S x 128, S = the largest
  *    batch slice of one launch for this act_bits, min(32, 64 / act_bits)]
  *                                             zero on entry, left zero

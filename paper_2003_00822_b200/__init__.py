@@ -50,6 +50,8 @@ _SIGS = {
     "pb_quantize_pack_weights": ([_p, _i64, _i64, _i32, _i32, _f32, _p, _i32, _p, _W], _i32),
     "pb_quantize_pack_weights_step": ([_p, _i64, _i64, _i32, _dbl, _p, _i32, _p, _W], _i32),
     "pb_pack_codes": ([_p, _i64, _i64, _i32, _i32, _dbl, _p, _i32, _p, _W], _i32),
+    "pb_pack_device_workspace_bytes": ([], _sz),
+    "pb_quantize_pack_weights_device": ([_p, _i64, _i64, _i32, _f32, _dbl, _p, _p, _sz, _p, _W], _i32),
     "pb_search_clip": ([_p, _i64, _i64, _i32, C.POINTER(_f32)], _i32),
     "pb_workspace_bytes": ([_i64, _i64, _i32], _sz),
     "pb_act_quantize": ([_p, _i64, _i64, _i32, _i32, _p, _sz, _p], _i32),
@@ -159,6 +161,22 @@ class PackedWeights:
         d = pb_weights()
         st = pb_quantize_pack_weights(_ptr(W), rows, cols, L, mode, float(clip), _ptr(buf),
                                       1 if buf.is_cuda else 0, None, C.byref(d))
+        check(st, (PB_OK, PB_EDEGENERATE))
+        return cls(buf, d, st)
+
+    @classmethod
+    def quantize_device(cls, W, L, clip=0.0, step=0.0):
+        """pb_quantize_pack_weights_device: W a device float32 tensor [rows][cols] (PB_Q_GRID,
+        or the given grid step); same bytes and scale as quantize / quantize_step."""
+        import torch
+        assert W.is_cuda and W.dtype == torch.float32 and W.dim() == 2
+        W = W.contiguous()
+        rows, cols = W.shape
+        buf = cls._alloc(rows, cols, L, W.device)
+        ws = torch.empty(max(16, pb_pack_device_workspace_bytes()), dtype=torch.uint8, device=W.device)
+        d = pb_weights()
+        st = pb_quantize_pack_weights_device(W.data_ptr(), rows, cols, L, float(clip), float(step), _ptr(buf),
+                                             ws.data_ptr(), ws.numel(), _stream(None), C.byref(d))
         check(st, (PB_OK, PB_EDEGENERATE))
         return cls(buf, d, st)
 

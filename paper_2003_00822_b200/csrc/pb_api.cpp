@@ -324,6 +324,72 @@ pb_status pb_quantize_pack_weights(const float* W_host, int64_t rows, int64_t co
     return PB_OK;
 }
 
+size_t pb_pack_device_workspace_bytes(void) { return pb::align_up(sizeof(float) * 2 * pb::kPackBlocks); }
+
+pb_status pb_quantize_pack_weights_device(const float* W_dev, int64_t rows, int64_t cols, int32_t layers,
+                                          float clip, double step, void* dst, void* ws, size_t ws_bytes,
+                                          pb_stream s, pb_weights* out) {
+    g_err[0] = 0;
+    if (!out) return fail(PB_EINVAL, "out is NULL");
+    if (rows < 0 || cols < 0) return fail(PB_EINVAL, "negative rows/cols");
+    if (layers < 2 || layers > 16) return fail(PB_EINVAL, "layers=%d not in [2,16] (PB_Q_GRID)", layers);
+    if (step < 0.0 || !std::isfinite(step)) return fail(PB_EINVAL, "step must be 0 (from the extrema) or > 0");
+    const int64_t n = rows * cols;
+    if (n > 0 && !W_dev) return fail(PB_EINVAL, "W_dev is NULL");
+    if (pb_packed_bytes(rows, cols, layers) > 0 && (!dst || !aligned(dst, 16)))
+        return fail(PB_EINVAL, "dst must be non-NULL and 16-byte aligned");
+    if (step == 0.0 && n > 0 && (!ws || !aligned(ws, 16) || ws_bytes < pb_pack_device_workspace_bytes()))
+        return fail(PB_EINVAL, "workspace < pb_pack_device_workspace_bytes()");
+    const cudaStream_t cs = static_cast<cudaStream_t>(s);
+    double d = step;
+    bool deg = false, all_zero = false;
+    if (n == 0) {
+        d = 1.0;
+        deg = true;
+    } else if (step == 0.0) {
+        // Q(W) grid from the exact float extrema (clip is monotonic: applied after)
+        int blocks = (int)((n + 256 * 64 - 1) / (256 * 64));
+        blocks = blocks < 1 ? 1 : (blocks > pb::kPackBlocks ? pb::kPackBlocks : blocks);
+        float* part = static_cast<float*>(ws);
+        cudaError_t e = pb::launch_minmax(W_dev, n, part, blocks, cs);
+        std::vector<float> h((size_t)2 * blocks);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), part, sizeof(float) * h.size(), cudaMemcpyDeviceToHost, cs);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+        if (e != cudaSuccess) return cuda_fail(e, "pack: min/max");
+        float fmn = INFINITY, fmx = -INFINITY;
+        for (int b = 0; b < blocks; ++b) {
+            fmn = std::fmin(fmn, h[2 * b]);
+            fmx = std::fmax(fmx, h[2 * b + 1]);
+        }
+        const double mn = clipv((double)fmn, clip), mx = clipv((double)fmx, clip);
+        d = grid_step(mn, mx, layers - 1, deg);
+        all_zero = deg && mx == 0.0 && mn == 0.0;
+    }
+    if (n > 0) {
+        cudaError_t e = pb::launch_pack_grid(W_dev, rows, cols, pb_kwords(cols), layers, d,
+                                             step == 0.0 ? (double)clip : 0.0, all_zero ? 1 : 0,
+                                             static_cast<uint32_t*>(dst), cs);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+        if (e != cudaSuccess) return cuda_fail(e, "pack: bitlayers");
+    } else if (pb_packed_bytes(rows, cols, layers) > 0) {
+        cudaError_t e = cudaMemsetAsync(dst, 0, pb_packed_bytes(rows, cols, layers), cs);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+        if (e != cudaSuccess) return cuda_fail(e, "pack: zero fill");
+    }
+    out->bits = static_cast<uint32_t*>(dst);
+    out->rows = rows;
+    out->cols = cols;
+    out->kwords = pb_kwords(cols);
+    out->layers = layers;
+    out->offset = 0;
+    out->scale = all_zero ? 1.0 : d;
+    if (deg && step == 0.0) {
+        fail(PB_EDEGENERATE, "max(W) == min(W): degenerate grid (reading G5)");
+        return PB_EDEGENERATE;
+    }
+    return PB_OK;
+}
+
 pb_status pb_quantize_pack_weights_step(const float* W_host, int64_t rows, int64_t cols, int32_t layers,
                                         double step, void* dst, int32_t dst_is_device, pb_stream s,
                                         pb_weights* out) {

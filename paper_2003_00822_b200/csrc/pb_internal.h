@@ -139,6 +139,10 @@ cudaError_t launch_lstm_cell(const float* gates, const float* c, int64_t B, int6
                              float* h_out, float* c_out, cudaStream_t s);
 cudaError_t launch_lstm_cell_ilv(const float* gates, const float* c, int64_t B, int64_t H,
                                  float* h_out, float* c_out, cudaStream_t s);
+cudaError_t launch_minmax(const float* W, int64_t n, float* partial, int blocks, cudaStream_t s);
+cudaError_t launch_pack_grid(const float* W, int64_t R, int64_t K, int64_t kw, int L, double d, double clip,
+                             int all_zero, uint32_t* dst, cudaStream_t s);
+constexpr int kPackBlocks = 1024;    // pb_quantize_pack_weights_device: min/max partial blocks
 cudaError_t launch_rnn_cell(const float* gates, int64_t B, int64_t H, float* h_out,
                             cudaStream_t s);
 cudaError_t launch_permute_shards(const float* gathered, int64_t B, int64_t rows_per_rank,
