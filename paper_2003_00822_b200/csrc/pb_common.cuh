@@ -35,33 +35,16 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  "r"(bytes)
                  : "memory");
 }
-#ifndef PB_WAIT_HINT
-#define PB_WAIT_HINT 0
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    if (PB_WAIT_HINT > 0) {
-        // suspend-time hint (ns): a waiting thread sleeps until the phase completes instead of
-        // re-polling, leaving the issue slots to the warps doing work
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "WAIT_%=:\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-            "@!p bra WAIT_%=;\n"
-            "}\n" ::"r"(smem_u32(bar)),
-            "r"(parity), "n"(PB_WAIT_HINT)
-            : "memory");
-    } else {
-        asm volatile(
-            "{\n"
-            ".reg .pred p;\n"
-            "WAIT_%=:\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-            "@!p bra WAIT_%=;\n"
-            "}\n" ::"r"(smem_u32(bar)),
-            "r"(parity)
-            : "memory");
-    }
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -624,10 +624,17 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             smem_u32(&bars.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = bars.tmem_base;
+    // warp 0 (whose thread 0 initialised the barriers) only arrives: its weight tiles start
+    // streaming now, while the other warps wait for the TMEM allocation and the scale factors
+    if (warp == 0) {
+        __syncwarp();
+        asm volatile("bar.arrive 8, %0;" ::"n"(kThreads) : "memory");
+    } else {
+        tc_fence_before();
+        asm volatile("bar.sync 8, %0;" ::"n"(kThreads) : "memory");
+        tc_fence_after();
+    }
+    const uint32_t tmem = warp == 0 ? 0u : bars.tmem_base;
     if (warp >= kConv0 && warp < kConv0 + 4) {
         // E8M0 block scale factors: columns 0..3 = 1.0 (SFA), columns 4(1+s)..4(1+s)+3 = 2^s
         // (SFB of passes with in-group weight 2^s); every byte of a column holds the same value
@@ -648,9 +655,11 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         }
         tmem_st_wait();
     }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+    if (warp != 0) {
+        tc_fence_before();
+        asm volatile("bar.sync 9, %0;" ::"n"(kThreads - 32) : "memory");
+        tc_fence_after();
+    }
     pdl_trigger();
 
     int qi = 0;                 // work-item queue position (every role walks the same items)

@@ -15,7 +15,8 @@ ap.add_argument("--K", type=int, default=16384)
 ap.add_argument("--B", type=int, default=1)
 ap.add_argument("--a", type=int, default=16)
 ap.add_argument("--L", type=int, nargs="+", default=[1, 2, 4, 8, 16])
-ap.add_argument("--steps", type=int, default=60)
+ap.add_argument("--steps", type=int, default=64)
+ap.add_argument("--per", type=int, default=8, help="calls per CUDA graph (back to back, PDL-chained)")
 args = ap.parse_args()
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
 x = torch.randn(args.B, args.K, device="cuda")
@@ -36,22 +37,25 @@ for L in args.L:
         for w in cp:
             pb.matmul(x, w, L, args.a, y=y, ws=ws, stream=s)
     torch.cuda.synchronize()
-    gs = []
-    for w in cp:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=s):
-            pb.matmul(x, w, L, args.a, y=y, ws=ws, stream=s)
-        gs.append(g)
-    for i in range(6):
-        gs[i % M].replay()
+    M = max(M, 2)
+    while len(cp) < M:
+        cp.append(w0.clone_to(torch.empty_like(w0.buf)))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for t in range(args.per):
+            pb.matmul(x, cp[t % M], L, args.a, y=y, ws=ws, stream=s)
+    reps = max(1, args.steps // args.per)
+    for i in range(2):
+        g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    for i in range(args.steps):
-        gs[i % M].replay()
+    for i in range(reps):
+        g.replay()
     e1.record()
     torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) * 1e3 / args.steps
+    us = e0.elapsed_time(e1) * 1e3 / (reps * args.per)
+    gs = [g]
     gbs = (L * args.R * args.K / 8 + 4 * args.B * (args.K + args.R)) / us / 1e3
     out.append(f"L={L}:{us:.1f}us/{gbs:.0f}GB/s")
     del gs, cp, w0
