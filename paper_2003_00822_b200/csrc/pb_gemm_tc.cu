@@ -414,8 +414,9 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     const float xv0 = (i0 + ew < i1) ? item_x(i0 + ew) : 0.f;
     const float xv1 = (i0 + ew + kEpiWarps < i1) ? item_x(i0 + ew + kEpiWarps) : 0.f;
     // ---- a1 (part 1): max|x[b,:]|
+    // (a literal act_frac -- Alg. 2's fixed 2^16 cast, P:195 -- needs no max)
     const bool vec = (g.K & 3) == 0 && (reinterpret_cast<uintptr_t>(g.x) & 15) == 0;
-    for (int b = 0; b < B; ++b) {
+    for (int b = 0; b < (g.act_frac == kActAutoFrac ? B : 0); ++b) {
         const float* xb = g.x + (int64_t)b * g.K;
         float m = 0.f;
         if (vec) {

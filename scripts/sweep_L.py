@@ -16,6 +16,7 @@ ap.add_argument("--B", type=int, default=1)
 ap.add_argument("--a", type=int, default=16)
 ap.add_argument("--L", type=int, nargs="+", default=[1, 2, 4, 8, 16])
 ap.add_argument("--steps", type=int, default=64)
+ap.add_argument("--act-frac", type=int, default=-1024, help="PB_ACT_AUTO (-1024) or a literal f")
 ap.add_argument("--per", type=int, default=8, help="calls per CUDA graph (back to back, PDL-chained)")
 args = ap.parse_args()
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -35,7 +36,7 @@ for L in args.L:
     cp = [w0] + [w0.clone_to(torch.empty_like(w0.buf)) for _ in range(M - 1)]
     with torch.cuda.stream(s):
         for w in cp:
-            pb.matmul(x, w, L, args.a, y=y, ws=ws, stream=s)
+            pb.matmul(x, w, L, args.a, args.act_frac, y=y, ws=ws, stream=s)
     torch.cuda.synchronize()
     M = max(M, 2)
     while len(cp) < M:
@@ -43,7 +44,7 @@ for L in args.L:
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         for t in range(args.per):
-            pb.matmul(x, cp[t % M], L, args.a, y=y, ws=ws, stream=s)
+            pb.matmul(x, cp[t % M], L, args.a, args.act_frac, y=y, ws=ws, stream=s)
     reps = max(1, args.steps // args.per)
     for i in range(2):
         g.replay()
