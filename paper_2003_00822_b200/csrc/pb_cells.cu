@@ -12,7 +12,6 @@
 namespace pb {
 namespace {
 
-__device__ __forceinline__ float sigm(float v) { return sigmoidf_(v); }
 
 __global__ void lstm_cell_kernel(const float* __restrict__ gates, const float* __restrict__ c,
                                  int64_t B, int64_t H, float* __restrict__ h_out,

@@ -358,11 +358,6 @@ __device__ __forceinline__ void grid_wait(const int* ctr, unsigned long long bas
     while (ld_acquire_gpu_u64(c) < base + kGridStride) {
     }
 }
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 // Fused steps a1-a2 (same arithmetic as pb_act.cu), run at
 // kernel start by the 4 epilogue warps (128 threads, bar 5; idle until their first
 // segment) while warp 0 streams weight tiles and the converters already build A
