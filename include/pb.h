@@ -292,6 +292,35 @@ pb_status pb_comm_unique_id(void* id128);
 pb_status pb_comm_init(pb_comm** comm, const void* id128, int32_t nranks, int32_t rank);
 pb_status pb_comm_destroy(pb_comm* comm);
 
+/* Fused row-shard all-gather over peer memory (a6 without NCCL).
+ * One process per GPU, ranks 1, 2, 4 or 8 of one node.  pb_p2p_create
+ * allocates this rank's library-owned buffer [256 B arrival counter][y_full
+ * batch x rows_total float32] and writes its CUDA IPC handle
+ * (pb_p2p_handle_bytes()); the caller all-gathers the handles in rank order
+ * (e.g. torch.distributed) and calls pb_p2p_open.  pb_matmul_rowshard_p2p runs
+ * a1-a5 on this rank's shard (w_shard rows = ceil(R/N), padded) in ONE fused
+ * tensor-engine launch whose finalisation stores each y row straight into
+ * every rank's y_full over NVLink (IPC mappings; the same buffer layout on
+ * every rank) and then joins a cross-rank barrier on the arrival counters
+ * (red.release.sys / ld.acquire.sys), so when the kernel completes on any rank
+ * its y_full holds all R rows -- bit-identical to pb_matmul on the whole layer.
+ * Stream-ordered; the same call sequence on every rank.  PB_EINVAL when the
+ * shape is outside the tensor engine's fused path (use pb_matmul_rowshard). */
+typedef struct pb_p2p pb_p2p;
+size_t pb_p2p_handle_bytes(void);
+pb_status pb_p2p_create(pb_p2p** p2p, int32_t nranks, int32_t rank, int64_t batch,
+                        int64_t rows_total, void* handle_out);
+pb_status pb_p2p_open(pb_p2p* p2p, const void* handles /* nranks x pb_p2p_handle_bytes() */);
+/* In-process alternative to pb_p2p_open (one process driving several GPUs with
+ * peer access enabled, or several ranks on one GPU): all[q] is rank q's object. */
+pb_status pb_p2p_open_peers(pb_p2p* p2p, pb_p2p* const* all);
+float* pb_p2p_y(pb_p2p* p2p);               /* device [batch][rows_total] */
+pb_status pb_p2p_destroy(pb_p2p* p2p);
+pb_status pb_matmul_rowshard_p2p(const float* x, int64_t batch, const pb_weights* w_shard,
+                                 int64_t rows_total, int32_t k_used, int32_t act_bits,
+                                 int32_t act_frac, pb_p2p* p2p, void* ws, size_t ws_bytes,
+                                 pb_stream s);
+
 /* Extra workspace for pb_matmul_rowshard: gather buffer [N][batch][ceil(R/N)]. */
 size_t pb_rowshard_workspace_bytes(int64_t batch, int64_t cols, int32_t act_bits,
                                    int64_t rows_total, int32_t nranks);

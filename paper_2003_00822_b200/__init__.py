@@ -71,6 +71,13 @@ _SIGS = {
     "pb_comm_destroy": ([_p], _i32),
     "pb_rowshard_workspace_bytes": ([_i64, _i64, _i32, _i64, _i32], _sz),
     "pb_matmul_rowshard": ([_p, _i64, _W, _i64, _i32, _i32, _i32, _p, _p, _p, _sz, _p], _i32),
+    "pb_p2p_handle_bytes": ([], _sz),
+    "pb_p2p_create": ([C.POINTER(_p), _i32, _i32, _i64, _i64, _p], _i32),
+    "pb_p2p_open": ([_p, _p], _i32),
+    "pb_p2p_open_peers": ([_p, C.POINTER(_p)], _i32),
+    "pb_p2p_y": ([_p], _p),
+    "pb_p2p_destroy": ([_p], _i32),
+    "pb_matmul_rowshard_p2p": ([_p, _i64, _W, _i64, _i32, _i32, _i32, _p, _p, _sz, _p], _i32),
 }
 for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -365,6 +372,64 @@ def matmul_rowshard(x, w_shard: PackedWeights, rows_total, comm: Comm, k_used=No
     check(pb_matmul_rowshard(_ptr(x), B, C.byref(w_shard.desc), rows_total, k_used or w_shard.layers, act_bits,
                              act_frac, _ptr(y_full), comm.handle, ws.ptr, ws.nbytes, _stream(stream)))
     return y_full
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of library-owned device memory (zero copy)."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 2, "strides": None}
+
+
+class P2P:
+    """Fused row-shard all-gather over peer memory (pb_p2p_*, pb_matmul_rowshard_p2p).
+    Every rank constructs it with the same (batch, rows_total); the IPC handles are
+    all-gathered over torch.distributed (any backend)."""
+
+    def __init__(self, batch, rows_total, nranks=None, rank=None, exchange=True):
+        import torch
+        import torch.distributed as dist
+        nranks = dist.get_world_size() if nranks is None else nranks
+        rank = dist.get_rank() if rank is None else rank
+        self.batch, self.rows_total, self.nranks, self.rank = batch, rows_total, nranks, rank
+        hb = int(pb_p2p_handle_bytes())
+        h = C.create_string_buffer(hb)
+        self.handle = C.c_void_p()
+        check(pb_p2p_create(C.byref(self.handle), nranks, rank, batch, rows_total, h))
+        if exchange:
+            mine = bytes(h.raw)
+            allh = [None] * nranks
+            dist.all_gather_object(allh, mine)
+            self._handles = C.create_string_buffer(b"".join(allh), hb * nranks)
+            check(pb_p2p_open(self.handle, self._handles))
+        self.y = torch.as_tensor(_DevArray(pb_p2p_y(self.handle), (batch, rows_total)), device="cuda")
+
+    @staticmethod
+    def in_process(batch, rows_total, nranks):
+        """All ranks' objects in this process (pb_p2p_open_peers), e.g. ranks sharing one GPU."""
+        objs = [P2P(batch, rows_total, nranks, r, exchange=False) for r in range(nranks)]
+        arr = (C.c_void_p * nranks)(*[o.handle.value for o in objs])
+        for o in objs:
+            check(pb_p2p_open_peers(o.handle, arr))
+        return objs
+
+    def close(self):
+        if self.handle:
+            self.y = None
+            pb_p2p_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+def matmul_rowshard_p2p(x, w_shard: PackedWeights, rows_total, p2p: P2P, k_used=None, act_bits=16,
+                        act_frac=PB_ACT_AUTO, ws=None, stream=None):
+    """y_full (= p2p.y, [B][rows_total], on every rank) of this rank's shard, gathered in the kernel."""
+    B = x.shape[0]
+    if ws is None:
+        ws = Workspace(workspace_bytes(B, w_shard.cols, act_bits), x.device)
+    check(pb_matmul_rowshard_p2p(_ptr(x), B, C.byref(w_shard.desc), rows_total, k_used or w_shard.layers, act_bits,
+                                 act_frac, p2p.handle, ws.ptr, ws.nbytes, _stream(stream)))
+    return p2p.y
 
 
 def shard_codes(codes, nranks, rank, offset=0):

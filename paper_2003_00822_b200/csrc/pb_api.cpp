@@ -510,9 +510,19 @@ struct CellOut {
     float* c_out;       // [B][H]
 };
 
+// Fused all-gather operands of pb_matmul_rowshard_p2p (GemmArgs nranks > 0), or null.
+struct P2POut {
+    int nranks;
+    int64_t R_total, row0;
+    float* peer_y[pb::kMaxRanks];
+    unsigned long long* peer_ctr[pb::kMaxRanks];
+    unsigned long long* local_ctr;
+};
+
 static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
                           float* y, int64_t* acc, const float* bias, int32_t fn, int32_t accumulate, pb_stream s,
-                          const float* x, int32_t act_frac, bool* fused_done, const CellOut* cell = nullptr) {
+                          const float* x, int32_t act_frac, bool* fused_done, const CellOut* cell = nullptr,
+                          const P2POut* p2p = nullptr) {
     if (fused_done) *fused_done = false;
 
     const pb::WsLayout l = pb::ws_layout(batch, w->kwords, act_bits);
@@ -552,6 +562,14 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     g.cell_c = nullptr;
     g.cell_h = nullptr;
     g.cell_c_out = nullptr;
+    g.nranks = 0;
+    g.R_total = 0;
+    g.row0 = 0;
+    for (int q = 0; q < pb::kMaxRanks; ++q) {
+        g.peer_y[q] = nullptr;
+        g.peer_ctr[q] = nullptr;
+    }
+    g.local_ctr = nullptr;
 
     cudaError_t e;
     const cudaStream_t cs = static_cast<cudaStream_t>(s);
@@ -581,6 +599,16 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
             gs.acc = acc ? reinterpret_cast<long long*>(acc) + b0 * w->rows : nullptr;
             gs.f = g.f + b0;
             gs.xsum = g.xsum + b0 * pb::kXsumStride;
+            if (p2p) {
+                gs.nranks = p2p->nranks;
+                gs.R_total = p2p->R_total;
+                gs.row0 = p2p->row0;
+                for (int q = 0; q < p2p->nranks; ++q) {
+                    gs.peer_y[q] = p2p->peer_y[q] + b0 * p2p->R_total;
+                    gs.peer_ctr[q] = p2p->peer_ctr[q];
+                }
+                gs.local_ctr = p2p->local_ctr;
+            }
             if (cell) {
                 gs.cell = 1;
                 gs.H = cell->H;
@@ -594,7 +622,7 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
         *fused_done = true;
         return PB_OK;
     }
-    if (cell) return PB_EINVAL;                  // the cell is fused on the tensor engine's fused path only
+    if (cell || p2p) return PB_EINVAL;           // cell / peer all-gather: the tensor engine's fused path only
     if (g_engine == PB_ENGINE_MMA) {
         if (!pb::tc_supported(g))
             return fail(PB_EINVAL, "PB_ENGINE_MMA on the split path needs act_bits*batch <= 64, batch <= 32 "
@@ -938,6 +966,130 @@ pb_status pb_matmul_rowshard(const float* x, int64_t batch, const pb_weights* w_
     cudaError_t e = pb::launch_permute_shards(gathered, batch, rs, N, rows_total, y_full, cs);
     if (e != cudaSuccess) return cuda_fail(e, "permute launch");
     return PB_OK;
+}
+
+// ------------------------------------------------------------ fused peer all-gather (f2)
+struct pb_p2p {
+    int nranks = 0, rank = 0;
+    int64_t batch = 0, rows_total = 0;
+    char* local = nullptr;                  // [counter: 256 B][y_full: batch x rows_total float32]
+    char* peer[pb::kMaxRanks] = {};         // opened IPC mappings (own rank: local)
+    bool opened = false;
+    bool borrowed = false;                  // peers opened in-process (pb_p2p_open_peers): nothing to close
+};
+
+static size_t p2p_bytes(int64_t batch, int64_t rows_total) {
+    return 256 + pb::align_up(sizeof(float) * (size_t)batch * (size_t)rows_total);
+}
+
+pb_status pb_p2p_create(pb_p2p** out, int32_t nranks, int32_t rank, int64_t batch, int64_t rows_total,
+                        void* handle_out) {
+    g_err[0] = 0;
+    if (!out || !handle_out) return fail(PB_EINVAL, "out/handle_out is NULL");
+    if (nranks < 1 || nranks > pb::kMaxRanks || (nranks & (nranks - 1)))
+        return fail(PB_EINVAL, "nranks=%d: 1, 2, 4 or 8 ranks of one node", nranks);
+    if (rank < 0 || rank >= nranks) return fail(PB_EINVAL, "rank=%d not in [0,%d)", rank, nranks);
+    if (batch < 1 || rows_total < 1) return fail(PB_EINVAL, "batch and rows_total must be >= 1");
+    pb_p2p* p = new pb_p2p;
+    p->nranks = nranks;
+    p->rank = rank;
+    p->batch = batch;
+    p->rows_total = rows_total;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->local), p2p_bytes(batch, rows_total));
+    if (e == cudaSuccess) e = cudaMemset(p->local, 0, p2p_bytes(batch, rows_total));
+    cudaIpcMemHandle_t h;
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p->local);
+    if (e != cudaSuccess) {
+        if (p->local) cudaFree(p->local);
+        delete p;
+        return cuda_fail(e, "p2p buffer / IPC handle");
+    }
+    std::memcpy(handle_out, &h, sizeof h);
+    *out = p;
+    return PB_OK;
+}
+
+size_t pb_p2p_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+pb_status pb_p2p_open(pb_p2p* p, const void* handles) {
+    g_err[0] = 0;
+    if (!p || !handles) return fail(PB_EINVAL, "p2p/handles is NULL");
+    if (p->opened) return PB_OK;
+    for (int q = 0; q < p->nranks; ++q) {
+        if (q == p->rank) {
+            p->peer[q] = p->local;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char*>(handles) + (size_t)q * sizeof h, sizeof h);
+        void* ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+        p->peer[q] = static_cast<char*>(ptr);
+    }
+    p->opened = true;
+    return PB_OK;
+}
+
+pb_status pb_p2p_open_peers(pb_p2p* p, pb_p2p* const* all) {
+    g_err[0] = 0;
+    if (!p || !all) return fail(PB_EINVAL, "p2p/all is NULL");
+    if (p->opened) return PB_OK;
+    for (int q = 0; q < p->nranks; ++q) {
+        if (!all[q] || all[q]->nranks != p->nranks || all[q]->rank != q || all[q]->batch != p->batch ||
+            all[q]->rows_total != p->rows_total)
+            return fail(PB_EINVAL, "peer %d does not match (nranks, rank, batch, rows_total)", q);
+        p->peer[q] = all[q]->local;
+    }
+    p->opened = true;
+    p->borrowed = true;
+    return PB_OK;
+}
+
+float* pb_p2p_y(pb_p2p* p) { return p ? reinterpret_cast<float*>(p->local + 256) : nullptr; }
+
+pb_status pb_p2p_destroy(pb_p2p* p) {
+    if (!p) return PB_OK;
+    cudaDeviceSynchronize();
+    for (int q = 0; q < p->nranks; ++q)
+        if (p->peer[q] && q != p->rank && !p->borrowed) cudaIpcCloseMemHandle(p->peer[q]);
+    if (p->local) cudaFree(p->local);
+    delete p;
+    return PB_OK;
+}
+
+pb_status pb_matmul_rowshard_p2p(const float* x, int64_t batch, const pb_weights* w_shard, int64_t rows_total,
+                                 int32_t k_used, int32_t act_bits, int32_t act_frac, pb_p2p* p, void* ws,
+                                 size_t ws_bytes, pb_stream s) {
+    g_err[0] = 0;
+    if (!p || !p->opened) return fail(PB_EINVAL, "p2p is NULL or not opened (pb_p2p_open)");
+    if (batch != p->batch || rows_total != p->rows_total)
+        return fail(PB_EINVAL, "batch/rows_total differ from the p2p buffer's");
+    pb_status st = validate_gemm(ws, ws_bytes, batch, w_shard, k_used, act_bits, pb_p2p_y(p), nullptr, PB_FN_NONE);
+    if (st != PB_OK) return st;
+    if ((st = check_act(batch, w_shard->cols, act_bits, act_frac)) != PB_OK) return st;
+    const int N = p->nranks;
+    const int64_t rs = (rows_total + N - 1) / N;
+    if (w_shard->rows != rs)
+        return fail(PB_EINVAL, "shard rows %lld != ceil(R/N) = %lld (pad the last shards with zero rows)",
+                    (long long)w_shard->rows, (long long)rs);
+    if (!x || !aligned(x, 4)) return fail(PB_EINVAL, "x must be a non-NULL device pointer");
+    P2POut po;
+    po.nranks = N;
+    po.R_total = rows_total;
+    po.row0 = rs * p->rank;
+    for (int q = 0; q < N; ++q) {
+        po.peer_y[q] = reinterpret_cast<float*>(p->peer[q] + 256);
+        po.peer_ctr[q] = reinterpret_cast<unsigned long long*>(p->peer[q]);
+    }
+    po.local_ctr = reinterpret_cast<unsigned long long*>(p->local);
+    bool fused = false;
+    st = run_gemm(ws, batch, w_shard, k_used, act_bits, nullptr, nullptr, nullptr, PB_FN_NONE, 0, s, x, act_frac,
+                  &fused, nullptr, &po);
+    if (st == PB_OK && !fused) st = PB_EINVAL;
+    if (st == PB_EINVAL && !g_err[0])
+        return fail(PB_EINVAL, "the fused peer all-gather needs the tensor engine's fused path for this shape");
+    return st;
 }
 
 }  // extern "C"

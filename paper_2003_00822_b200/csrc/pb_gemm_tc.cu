@@ -346,6 +346,25 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned 
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// Cross-rank wait (f2): spin on an arrival counter other GPUs add to; a peer that never
+// arrives (a rank that died or diverged) ends the kernel with a trap after 30 s instead of
+// hanging the device.
+__device__ __forceinline__ void sys_wait(const unsigned long long* ctr, unsigned long long target) {
+    long long t0 = 0;
+    for (unsigned k = 0; ld_acquire_sys_u64(ctr) < target; ++k) {
+        if ((k & 1023) == 1023) {
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t0 == 0) t0 = t;
+            else if (t - t0 > 30000000000ll) asm volatile("trap;");
+        }
+    }
+}
 __device__ __forceinline__ unsigned long long grid_base(const int* ctr) {
     return ld_acquire_gpu_u64(reinterpret_cast<const unsigned long long*>(ctr)) & ~(kGridStride - 1);
 }
@@ -958,7 +977,17 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         };
         auto finish_tile_row = [&](int b, int64_t row, unsigned long long t) {   // warp-uniform call
             if (!g.cell) {
-                if (row < g.R) g.y[(int64_t)b * g.R + row] = apply_fn(preact(b, row, t), g.fn);
+                if (row < g.R) {
+                    const float v = apply_fn(preact(b, row, t), g.fn);
+                    if (g.nranks) {
+                        // fused all-gather (f2): this row of y into every rank's y_full
+                        const int64_t grow = g.row0 + row;
+                        if (grow < g.R_total)
+                            for (int q = 0; q < g.nranks; ++q) g.peer_y[q][(int64_t)b * g.R_total + grow] = v;
+                    } else {
+                        g.y[(int64_t)b * g.R + row] = v;
+                    }
+                }
                 return;
             }
             const float v = row < g.R ? preact(b, row, t) : 0.f;
@@ -980,6 +1009,21 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             pdl_wait();
         // end-of-work barrier base (after the PDL wait above: every earlier call is complete)
         const unsigned long long ebase = (ew == 0 && lane == 0) ? grid_base(g.ebar) : 0ull;
+        // cross-rank barrier base (f2): every rank's previous call has completed (its kernel
+        // waited for all ranks), and no rank can arrive for the next call before this one
+        unsigned long long xbase = 0, rbase = 0;
+        if (g.nranks && ew == 0 && lane == 0) {
+            xbase = ld_acquire_sys_u64(g.local_ctr) & ~(kGridStride - 1);
+            rbase = ld_acquire_sys_u64(g.local_ctr + 1) & ~(kGridStride - 1);
+            // entry handshake: this rank's stream has reached the call (everything before it,
+            // including readers of the previous y_full, is complete), so peers may now store
+            // into this rank's y_full -- CTA 0 tells every rank (ready counter, word 1)
+            if (blockIdx.x == 0)
+                for (int q = 0; q < g.nranks; ++q)
+                    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(g.peer_ctr[q] + 1),
+                                 "l"(kGridStride / (unsigned)g.nranks)
+                                 : "memory");
+        }
         int seg = 0;
         while (true) {
             const int2 it = take_item(bars, qi, qph, lane);
@@ -1079,6 +1123,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             if TLP(g) bars.t_ebar[0] = gtimer();
             grid_arrive(g.ebar);
             grid_wait(g.ebar, ebase);                // acquire; bar.sync passes it to the CTA
+            if (g.nranks)                            // every rank has entered this call (f2)
+                sys_wait(g.local_ctr + 1, rbase + kGridStride);
             if TLP(g) bars.t_ebar[1] = gtimer();
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -1090,6 +1136,22 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 ab[b * kTcRows] = 0;                  // every call leaves the accumulators zero
                 finish_tile_row(b, row, t);
             }
+        }
+        if (g.nranks) {
+            // every rank's y_full holds this CTA's rows once its counter has the arrival: each
+            // rank's CTAs add kGridStride / nranks in total (CTA 0 the remainder), so a call
+            // adds exactly kGridStride to every counter whatever the grid sizes
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (ew == 0 && lane == 0) {
+                __threadfence_system();              // the CTA's remote y stores (ordered by bar.sync)
+                const unsigned long long amt =
+                    blockIdx.x == 0 ? kGridStride / (unsigned)g.nranks - (gridDim.x - 1) : 1ull;
+                for (int q = 0; q < g.nranks; ++q)
+                    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(g.peer_ctr[q]), "l"(amt)
+                                 : "memory");
+                sys_wait(g.local_ctr, xbase + kGridStride);
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
         }
         if (TLP(g) && ew == 0 && lane == 0) bars.t_cend = gtimer();
     }

@@ -13,6 +13,7 @@ constexpr size_t kAlign = 256;
 constexpr int kTcRows = 128;         // tensor engine row tile (MMA M)
 constexpr int kTcMaxN = 64;          // tensor engine: a * batch <= 64 per launch (MMA N padded to 8/16/32/64)
 constexpr int kTcMaxB = 32;          // tensor engine: batch columns per launch
+constexpr int kMaxRanks = 8;         // pb_matmul_rowshard_p2p: ranks of one node
 
 inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
 
@@ -122,6 +123,15 @@ struct GemmArgs {
     const float* cell_c;          // [B][H] c_t
     float* cell_h;                // [B][H] h_{t+1}
     float* cell_c_out;            // [B][H] c_{t+1}
+    // fused row-shard all-gather over peer memory (pb_matmul_rowshard_p2p):
+    // the finalisation stores this shard's y rows straight into every rank's y_full
+    // [B][R_total] (IPC / NVLink P2P mappings); then every CTA adds to every rank's arrival
+    // counter (red.release.sys) and waits on its own: one cross-rank barrier, no NCCL
+    int nranks;                   // 0 = off
+    int64_t R_total, row0;        // global rows, this shard's first global row
+    float* peer_y[kMaxRanks];     // rank p's y_full (this slice's batch offset applied)
+    unsigned long long* peer_ctr[kMaxRanks];
+    unsigned long long* local_ctr;
 };
 
 // Diagnostics timeline (PB_TC_DEBUG=6): device log, [0] = record counter,

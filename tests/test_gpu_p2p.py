@@ -1,0 +1,70 @@
+"""Fused peer all-gather (pb_matmul_rowshard_p2p) with N ranks on
+ONE GPU in one process: each rank's fused kernel runs on its own stream with a grid
+small enough that all ranks' CTAs are resident together, and the ranks' buffers are
+joined with pb_p2p_open_peers.  The kernel's remote y stores, the cross-rank arrival
+counters (red.release.sys / ld.acquire.sys) and the entry handshake run as they do
+across NVLink; only the IPC mapping differs (pb_p2p_open, used by bench.py under
+torchrun).  Every rank's y_full must equal pb_matmul on the whole layer bit-exactly,
+over repeated calls (monotonic counters) and inside CUDA graphs."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb():
+    import build_pb
+    build_pb.build()
+    import paper_2003_00822_b200 as pb
+    return pb
+
+
+@pytest.mark.parametrize("N,R,K,L,B", [(2, 2048, 2048, 4, 1), (2, 1000, 784, 3, 3), (2, 4096, 4096, 8, 2),
+                                       (4, 2048, 1024, 5, 1), (8, 1030, 512, 2, 2), (2, 2048, 2048, 16, 4)])
+def test_p2p_ranks_on_one_gpu(pb, N, R, K, L, B):
+    import torch
+    m = synth.codes(R, K, L, 5 + N)
+    w_full = pb.PackedWeights.from_codes(m, L, 0, 0.25)
+    ws_ = [pb.PackedWeights.from_codes(pb.shard_codes(m, N, r), L, 0, 0.25) for r in range(N)]
+    p2ps = pb.P2P.in_process(B, R, N)
+    wss = [pb.Workspace(pb.workspace_bytes(B, K, 16)) for _ in range(N)]
+    streams = [torch.cuda.Stream() for _ in range(N)]
+    try:
+        for it in range(3):
+            x = torch.from_numpy(synth.activations(B, K, 6 + it)).cuda()
+            ref = pb.matmul(x, w_full, L, 16)
+            torch.cuda.synchronize()
+            for r in range(N):
+                pb.matmul_rowshard_p2p(x, ws_[r], R, p2ps[r], L, 16, ws=wss[r], stream=streams[r])
+            torch.cuda.synchronize()
+            for r in range(N):
+                assert torch.equal(p2ps[r].y.view(torch.int32), ref.view(torch.int32)), (it, r)
+        # CUDA graphs: 3 back-to-back calls per rank, one graph per rank.  Within a graph the
+        # next call's CTAs launch early (PDL) and take free SMs; on one GPU every rank's two
+        # calls in flight must fit (on separate GPUs they do by construction)
+        units = -(-R // N // 128) * -(-K // 1024)
+        if 2 * N * units > 148:
+            return
+        x = torch.from_numpy(synth.activations(B, K, 99)).cuda()
+        ref = pb.matmul(x, w_full, L, 16)
+        graphs = []
+        for r in range(N):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=streams[r]):
+                for _ in range(3):
+                    pb.matmul_rowshard_p2p(x, ws_[r], R, p2ps[r], L, 16, ws=wss[r], stream=streams[r])
+            graphs.append(g)
+        torch.cuda.synchronize()
+        for r in range(N):
+            with torch.cuda.stream(streams[r]):
+                graphs[r].replay()
+        torch.cuda.synchronize()
+        for r in range(N):
+            assert torch.equal(p2ps[r].y.view(torch.int32), ref.view(torch.int32)), ("graph", r)
+    finally:
+        torch.cuda.synchronize()
+        for p in p2ps:
+            p.close()
