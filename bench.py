@@ -55,6 +55,9 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="oracle cpu_baseline budget")
     p.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline (profiling runs)")
     p.add_argument("--no-compare", action="store_true", help="skip the cuBLAS fp32/bf16/int8 comparison (f3)")
+    p.add_argument("--allgather", default="auto", choices=["auto", "p2p", "nccl"],
+                   help="N > 1: fused peer all-gather in the kernel (p2p), NCCL, or p2p verified against NCCL "
+                        "at start with NCCL as the fallback (auto)")
     p.add_argument("--no-lstm", action="store_true", help="skip the LSTM-LM (configs[2]) sequence timing (f1)")
     p.add_argument("--ref-budget", type=float, default=120.0, help="--impl reference total budget (s)")
     return p.parse_args()
@@ -259,8 +262,32 @@ def main():
     ws = pb.Workspace(ws_bytes)
     stream = torch.cuda.Stream()
 
+    # N > 1: the all-gather fused into the kernel over peer memory, checked
+    # bit-exactly against the NCCL path once before timing; NCCL is the fallback
+    p2p, ag_note = None, "nccl"
+    if N > 1 and args.allgather in ("auto", "p2p"):
+        try:
+            p2p = pb.P2P(B, R)
+            pb.matmul_rowshard(x, copies[0], R, comm, k_used, a, y_full=y, ws=ws)
+            pb.matmul_rowshard_p2p(x, copies[0], R, p2p, k_used, a, ws=ws)
+            torch.cuda.synchronize()
+            bad = torch.tensor([0 if torch.equal(p2p.y.view(torch.int32), y.view(torch.int32)) else 1],
+                               device="cuda")
+            dist.all_reduce(bad, dist.ReduceOp.MAX)
+            if bad.item():
+                raise RuntimeError("fused p2p all-gather differs from NCCL")
+            ag_note = "fused p2p (kernel stores y rows into every rank's buffer; verified == NCCL)"
+        except Exception as e:
+            if args.allgather == "p2p":
+                raise
+            if p2p is not None:
+                p2p.close()
+            p2p, ag_note = None, f"nccl (p2p unavailable: {str(e)[:120]})"
+
     def step(w, s=None):
-        if N > 1:
+        if p2p is not None:
+            pb.matmul_rowshard_p2p(x, w, R, p2p, k_used, a, ws=ws, stream=s)
+        elif N > 1:
             pb.matmul_rowshard(x, w, R, comm, k_used, a, y_full=y, ws=ws, stream=s)
         else:
             pb.matmul(x, w, k_used, a, y=y, ws=ws, stream=s)
@@ -423,14 +450,18 @@ def main():
         cs.wait_event(ev_h2d[j])
         if i >= 2:
             cs.wait_event(ev_d2h[j])                    # y of step i-2 has left yb[j]
-        if N > 1:
+        if p2p is not None:
+            if i >= 1:
+                cs.wait_event(ev_d2h[j ^ 1])            # one library-owned y_full: step i-1's D2H first
+            pb.matmul_rowshard_p2p(xb[j], copies[i % M], R, p2p, k_used, a, ws=ws, stream=cs)
+        elif N > 1:
             pb.matmul_rowshard(xb[j], copies[i % M], R, comm, k_used, a, y_full=yb[j], ws=ws, stream=cs)
         else:
             pb.matmul(xb[j], copies[i % M], k_used, a, y=yb[j], ws=ws, stream=cs)
         ev_k[j].record(cs)
         with torch.cuda.stream(d2h_s):
             d2h_s.wait_event(ev_k[j])
-            y_hb[j].copy_(yb[j], non_blocking=True)
+            y_hb[j].copy_(p2p.y if p2p is not None else yb[j], non_blocking=True)
             ev_d2h[j].record(d2h_s)
 
     for i in range(4):
@@ -571,6 +602,8 @@ def main():
                "sample": f"{rows} of {R} rows (all {K} cols, L={L}, a={a}, B={B}) in {dt:.1f} s, "
                          f"OpenMP over rows"}
 
+    if p2p is not None:
+        p2p.close()
     if comm is not None:
         comm.close()
     if rank == 0:
@@ -581,11 +614,12 @@ def main():
                           if fused else "b1 (AND/popc) -> int32 counts -> int64"), "data": "synthetic",
                 "config": {"workload": WORKLOAD, "R": R, "K": K, "L": L, "k_used": k_used, "act_bits": a,
                            "batch": B, "parallelism": f"rowshard{N}" if N > 1 else "single",
+                           "allgather": ag_note if N > 1 else None,
                            "engine": args.engine, "weight_copies": M,
                            "l2": f"inputs larger than L2: {M} rotating weight copies, "
                                  f"{M * w0.nbytes() / 2**20:.0f} MiB >= 2x L2 ({l2 / 2**20:.0f} MiB)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": (launches_per_call + (1 if (N > 1 and B > 1) else 0)) * args.steps,
+                "gpu_launches": (launches_per_call + (1 if (N > 1 and B > 1 and p2p is None) else 0)) * args.steps,
                 "clocks": clocks, "per_L": per_L, "per_kused": per_k, "compare": compare, "lstm_lm": lstm,
                 "context": "paper: >8x end-to-end vs FP32 on a Tesla T4 (P:28, P:216) -- context, not target"}
         print(json.dumps(line), flush=True)
