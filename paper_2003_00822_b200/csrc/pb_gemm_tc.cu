@@ -96,6 +96,7 @@ struct Bars {
     uint64_t q_full[kQDepth], q_empty[kQDepth];
     int2 q[kQDepth];                          // work items: units [x, y); x < 0 = no more work
     uint64_t x_ready;                        // fused path: bars.xsum written (warp 2)
+    int fin_tile;                            // static schedule: shared tile this CTA completed (-1: none)
     uint64_t slice_done;                     // fused path: this CTA's slice of B written (epilogue warps)
     uint64_t pro_done;                       // fused path: first chunk's B built (converters resume)
     unsigned long long gbase;                // fused path: prologue grid-barrier counter base (grid_base)
@@ -291,12 +292,34 @@ struct TcPlan {
     int Gp;           // passes per accumulator group (<= G/2 layers pairs, K * 2^G <= 2^24)
     int regions;      // ceil(passes / Gp)
     int Gu;           // units per work item (dynamic claims)
+    int stat;         // static schedule: CTA i owns units [i*U/G, (i+1)*U/G) (one item each, no
+                      // claims); a segment covering a whole tile is finalised from its own sums, a
+                      // tile split between CTAs is summed exactly (red.add) and finalised by the
+                      // contributor that completes its chunk count -- no end-of-work barrier
     long long items;  // ceil(units / Gu)
     int dbg;          // profiling knob (env PB_TC_DEBUG): 1 = no A store, 2 = no MMA, 3 = neither,
                       // 6 = per-CTA timeline
     int prof;         // env PB_TC_PROF: print wait-cycle totals of CTA 0
 };
 
+// Units [u0, u1) of work item `item`: the static schedule splits the units evenly over
+// the grid (one item per CTA); the dynamic one hands out Gu units per claim.
+__device__ __forceinline__ void item_units(const TcPlan& p, long long item, long long& u0, long long& u1) {
+    if (p.stat) {
+        u0 = item * p.units / p.items;
+        u1 = (item + 1) * p.units / p.items;
+    } else {
+        u0 = item * p.Gu;
+        u1 = u0 + p.Gu;
+        if (u1 > p.units) u1 = p.units;
+    }
+}
+// K-chunk of the CTA's first (static) unit.
+__device__ __forceinline__ int first_kc(const TcPlan& p) {
+    long long u0, u1;
+    item_units(p, blockIdx.x, u0, u1);
+    return (int)(u0 % p.chunks);
+}
 // Least significant layer of pass ps (the pass's unit weight is |S_lo|).
 __device__ __host__ __forceinline__ int pass_lo(int k_used, int ps) {
     return (2 * ps + 1 < k_used) ? 2 * ps + 1 : 2 * ps;
@@ -689,9 +712,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         int tc = 0;
         while (true) {
             mbar_wait(&bars.q_empty[qi], qph ^ 1);
-            const long long u0 = item < p.items ? item * p.Gu : -1;
-            long long u1 = u0 + p.Gu;
-            if (u1 > p.units) u1 = p.units;
+            long long u0 = -1, u1 = 0;
+            if (item < p.items) item_units(p, item, u0, u1);
             if (lane == 0) {
                 bars.q[qi] = make_int2((int)u0, (int)u1);
                 mbar_arrive(&bars.q_full[qi]);
@@ -1004,7 +1026,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         };
         if (g.x)
             fused_prologue<NPAD>(g, p, bars, threadIdx.x - kEpi0 * 32, btile0,
-                                 (int)(((long long)blockIdx.x * p.Gu) % p.chunks));
+                                 first_kc(p));
         else
             pdl_wait();
         // end-of-work barrier base (after the PDL wait above: every earlier call is complete)
@@ -1096,11 +1118,44 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 // exact integer adds into the tile's accumulator (order-independent); no
                 // round trip here: tiles are finalised after the end-of-work grid barrier
                 unsigned long long* ab = g.accbuf + (int64_t)rt * g.B * kTcRows + m;
-                if (g.B == 1)
-                    red_add_u64(ab, tot1);
-                else
+                if (p.stat && kcA == 0 && kcB == p.chunks) {
+                    // static schedule, the segment is the whole tile: y straight from the sums
+                    const int64_t row = (int64_t)rt * kTcRows + m;
                     for (int b = 0; b < g.B; ++b)
-                        red_add_u64(ab + b * kTcRows, ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
+                        finish_tile_row(b, row,
+                                        g.B == 1 ? tot1 : ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
+                } else {
+                    if (g.B == 1) {
+                        red_add_u64(ab, tot1);
+                    } else {
+                        for (int b = 0; b < g.B; ++b)
+                            red_add_u64(ab + b * kTcRows, ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
+                    }
+                    if (p.stat) {
+                        // a tile shared with neighbouring CTAs (at most two per CTA): count its
+                        // chunks after the sums (the 128 threads' adds are ordered before thread
+                        // 0's acq_rel by bar.sync); the contributor that completes it finalises
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (ew == 0 && lane == 0) {
+                            int old;
+                            asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;"
+                                         : "=r"(old)
+                                         : "l"(g.counters + rt), "r"(kcB - kcA)
+                                         : "memory");
+                            bars.fin_tile = (old + (kcB - kcA) == p.chunks) ? rt : -1;
+                        }
+                        asm volatile("bar.sync 1, 128;" ::: "memory");
+                        if (bars.fin_tile >= 0) {
+                            const int64_t row = (int64_t)rt * kTcRows + m;
+                            for (int b = 0; b < g.B; ++b) {
+                                const unsigned long long t = __ldcg(ab + b * kTcRows);
+                                ab[b * kTcRows] = 0;       // every call leaves the accumulators zero
+                                finish_tile_row(b, row, t);
+                            }
+                            if (ew == 0 && lane == 0) g.counters[rt] = 0;
+                        }
+                    }
+                }
                 if (TLP(g) && ew == 0 && lane == 0) {
                     te[2] = gtimer();
                     bars.t_eseg[0] = te[0];
@@ -1118,6 +1173,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // ---- end-of-work grid barrier (the 128 threads' adds are ordered before the arrival by
         // bar.sync + thread 0's cumulative release), then this CTA finalises tiles
         // blockIdx.x, blockIdx.x + G, ...: y from the exact tile sums, accumulators re-zeroed
+        if (!p.stat) {
         asm volatile("bar.sync 1, 128;" ::: "memory");
         if (ew == 0 && lane == 0) {
             if TLP(g) bars.t_ebar[0] = gtimer();
@@ -1137,6 +1193,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 finish_tile_row(b, row, t);
             }
         }
+        }   // !p.stat
         if (g.nranks) {
             // every rank's y_full holds this CTA's rows once its counter has the arrival: each
             // rank's CTAs add kGridStride / nranks in total (CTA 0 the remainder), so a call
@@ -1260,6 +1317,7 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     // work items of >= ~4 passes (so an item's epilogue keeps up with its MMAs)
     if ((long long)g.B * p.chunks * kChunkWords >= (1ll << 31)) return false;   // prologue index math
     p.Gu = (4 + p.passes - 1) / p.passes;
+    p.stat = 0;
     p.items = (p.units + p.Gu - 1) / p.Gu;
     return true;
 }
@@ -1269,7 +1327,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 {
     static int sms = 0;
     static bool attr = false;
-    static int dbg = -1, prof = 0, bst_env = 0;
+    static int dbg = -1, prof = 0, bst_env = 0, stat_env = -1;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1280,6 +1338,8 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
         prof = ev ? atoi(ev) : 0;
         ev = getenv("PB_TC_BSTAGES");          // experiment knob: B ring depth
         bst_env = ev ? atoi(ev) : 0;
+        ev = getenv("PB_TC_STATIC");           // comparison knob: 0 = dynamic stream-K claims
+        stat_env = ev ? atoi(ev) : -1;
     }
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1291,6 +1351,11 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     }
     TcPlan p;
     if (!make_plan(g, NPAD, p)) return cudaErrorNotSupported;
+    if (stat_env != 0) {                       // default: static (PB_TC_STATIC=0: dynamic claims)
+        p.stat = 1;
+        p.items = p.units < sms ? p.units : sms;
+        if (p.items > kMaxCtas) p.items = kMaxCtas;
+    }
     CUtensorMap pmap, smap;
     cudaError_t e = make_weight_maps(g, &pmap, &smap);
     if (e != cudaSuccess) return e;
