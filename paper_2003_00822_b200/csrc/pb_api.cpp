@@ -622,7 +622,18 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
         *fused_done = true;
         return PB_OK;
     }
-    if (cell || p2p) return PB_EINVAL;           // cell / peer all-gather: the tensor engine's fused path only
+    if (p2p) return PB_EINVAL;                   // peer all-gather: the tensor engine's fused path only
+    if (cell) {                                  // the cell needs the tensor engine's finalisation
+        if (g_engine == PB_ENGINE_POPC || !pb::tc_supported(g)) return PB_EINVAL;
+        g.cell = 1;
+        g.H = cell->H;
+        g.cell_c = cell->c;
+        g.cell_h = cell->h_out;
+        g.cell_c_out = cell->c_out;
+        e = pb::launch_gemm_tc(g, cs);
+        if (e != cudaSuccess) return cuda_fail(e, "bitgemm (cell) launch");
+        return PB_OK;
+    }
     if (g_engine == PB_ENGINE_MMA) {
         if (!pb::tc_supported(g))
             return fail(PB_EINVAL, "PB_ENGINE_MMA on the split path needs act_bits*batch <= 64, batch <= 32 "
@@ -773,7 +784,15 @@ pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float*
                            act_ws, s)) != PB_OK)
         return st;
     // 2. per timestep: W_hh h_t + gx[t], then the cell -- fused into the tensor engine's
-    //    finalisation when the shape allows, else split (planes + GEMM + cell kernel)
+    //    finalisation when the shape allows (one launch for batch 1; planes kernel + GEMM when
+    //    a batch > 1 fits one tensor-engine launch: measured faster than the fused prologue's
+    //    per-column work), else planes + GEMM + cell kernel
+    static int split_env = -2;
+    if (split_env == -2) {
+        const char* ev = getenv("PB_LSTM_SPLIT");   // comparison knob: 0 = always fused, 1 = always split
+        split_env = ev ? atoi(ev) : -1;
+    }
+    const bool split_first = split_env >= 0 ? split_env > 0 : (batch > 1 && pb::tc_npad(batch, act_bits) > 0);
     for (int64_t t = 0; t < steps; ++t) {
         const float* h_in = t == 0 ? h0 : h_seq + (t - 1) * batch * H;
         const float* c_in = t == 0 ? c0 : (c_seq ? c_seq + (t - 1) * batch * H : cb[(t - 1) & 1]);
@@ -782,12 +801,23 @@ pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float*
         float* gt = gx + t * batch * 4 * H;
         const CellOut co{H, c_in, h_out, c_out};
         bool fused = false;
-        st = run_gemm(ws, batch, w_hh, k_used_hh, act_bits, gt, nullptr, nullptr, PB_FN_NONE, 1, s, h_in,
-                      PB_ACT_AUTO, &fused, &co);
-        if (st != PB_OK && st != PB_EINVAL) return st;
+        if (!split_first) {
+            st = run_gemm(ws, batch, w_hh, k_used_hh, act_bits, gt, nullptr, nullptr, PB_FN_NONE, 1, s, h_in,
+                          PB_ACT_AUTO, &fused, &co);
+            if (st != PB_OK && st != PB_EINVAL) return st;
+        }
         if (!fused) {
+            // planes by the activation kernel, then the tensor engine with the cell in its
+            // finalisation (batched h: the fused prologue's per-column work is the longer path)
             g_err[0] = 0;
             if ((st = pb_act_quantize(h_in, batch, H, act_bits, PB_ACT_AUTO, ws, act_ws, s)) != PB_OK) return st;
+            st = run_gemm(ws, batch, w_hh, k_used_hh, act_bits, gt, nullptr, nullptr, PB_FN_NONE, 1, s, nullptr, 0,
+                          nullptr, &co);
+            if (st != PB_OK && st != PB_EINVAL) return st;
+            fused = st == PB_OK;
+        }
+        if (!fused) {
+            g_err[0] = 0;                        // planes are in ws already: GEMM, then the cell kernel
             if ((st = run_gemm(ws, batch, w_hh, k_used_hh, act_bits, gt, nullptr, nullptr, PB_FN_NONE, 1, s, nullptr,
                                0, nullptr)) != PB_OK)
                 return st;
