@@ -292,6 +292,8 @@ struct TcPlan {
     int Gp;           // passes per accumulator group (<= G/2 layers pairs, K * 2^G <= 2^24)
     int regions;      // ceil(passes / Gp)
     int Gu;           // units per work item (dynamic claims)
+    int gs;           // static schedule: grid size; ustat: units split statically (the rest is
+    long long ustat;  // claimed dynamically, Gu per claim, to even out the CTAs' finishing times)
     int stat;         // static schedule: CTA i owns units [i*U/G, (i+1)*U/G) (one item each, no
                       // claims); a segment covering a whole tile is finalised from its own sums, a
                       // tile split between CTAs is summed exactly (red.add) and finalised by the
@@ -305,9 +307,13 @@ struct TcPlan {
 // Units [u0, u1) of work item `item`: the static schedule splits the units evenly over
 // the grid (one item per CTA); the dynamic one hands out Gu units per claim.
 __device__ __forceinline__ void item_units(const TcPlan& p, long long item, long long& u0, long long& u1) {
-    if (p.stat) {
-        u0 = item * p.units / p.items;
-        u1 = (item + 1) * p.units / p.items;
+    if (p.stat && item < p.gs) {
+        u0 = item * p.ustat / p.gs;
+        u1 = (item + 1) * p.ustat / p.gs;
+    } else if (p.stat) {                     // the dynamic tail: Gu units per claim
+        u0 = p.ustat + (item - p.gs) * p.Gu;
+        u1 = u0 + p.Gu;
+        if (u1 > p.units) u1 = p.units;
     } else {
         u0 = item * p.Gu;
         u1 = u0 + p.Gu;
@@ -1327,7 +1333,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 {
     static int sms = 0;
     static bool attr = false;
-    static int dbg = -1, prof = 0, bst_env = 0, stat_env = -1;
+    static int dbg = -1, prof = 0, bst_env = 0, stat_env = -1, dyn_pct = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1340,6 +1346,8 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
         bst_env = ev ? atoi(ev) : 0;
         ev = getenv("PB_TC_STATIC");           // comparison knob: 0 = dynamic stream-K claims
         stat_env = ev ? atoi(ev) : -1;
+        ev = getenv("PB_TC_DYN");              // experiment knob: % of units claimed dynamically
+        dyn_pct = ev ? atoi(ev) : 0;
     }
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1353,8 +1361,14 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     if (!make_plan(g, NPAD, p)) return cudaErrorNotSupported;
     if (stat_env != 0) {                       // default: static (PB_TC_STATIC=0: dynamic claims)
         p.stat = 1;
-        p.items = p.units < sms ? p.units : sms;
-        if (p.items > kMaxCtas) p.items = kMaxCtas;
+        p.gs = (int)(p.units < sms ? p.units : sms);
+        if (p.gs > kMaxCtas) p.gs = kMaxCtas;
+        long long dyn = p.units * dyn_pct / 100;   // a dynamic tail of single-unit claims
+        if (dyn < 0) dyn = 0;
+        p.Gu = 1;
+        p.ustat = p.units - dyn;
+        if (p.ustat < p.gs) p.ustat = p.units < p.gs ? p.units : p.gs;
+        p.items = p.gs + (p.units - p.ustat);
     }
     CUtensorMap pmap, smap;
     cudaError_t e = make_weight_maps(g, &pmap, &smap);
@@ -1369,7 +1383,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     if (p.wstages < 4) return cudaErrorNotSupported;
     const uint32_t smem = fixed + (uint32_t)p.wstages * kWTileBytes;
-    long long grid = p.items < sms ? p.items : sms;
+    long long grid = p.stat ? p.gs : (p.items < sms ? p.items : sms);
     if (grid > kMaxCtas) grid = kMaxCtas;
 
     cudaLaunchConfig_t cfg = {};
