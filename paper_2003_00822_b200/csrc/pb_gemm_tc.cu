@@ -19,38 +19,41 @@
 // Plane weights T_j, the group weights and the sign correction are applied in
 // the exact int64 epilogue, as in the POPC engine.
 //
-// Building A (per pair of words hi, lo and register r = 0..3, nibble e =
-// column 4e + r):  ((hi >> (r-1)) & 0x22222222) | ((lo >> r) & 0x11111111),
-// stored with tcgen05.st.32x32b (lane = row).
+// Building A from the paired storage (include/pb.h): each 2-bit field of a
+// stored pair word is already the e2m1 code 1.0*upper + 0.5*lower, so a register
+// of 8 nibbles is one mask (+ shift) of a stored word (build_a below), stored
+// with tcgen05.st.32x32b (lane = row).
 //
 // Why this shape (measured on B200, scripts/tc_mb.cu): an M=128
 // tcgen05 MMA costs ~55 cycles for any N <= 64 (an M=256 CTA-pair MMA costs the
 // same on two SMs), so weight bits per MMA set the rate: kind::i8 with byte
 // operands carries 32 bits per row, kind::mxf4 nibbles with one layer carry
-// 64, two stacked layers 128.  The issuing warp blocks on each MMA, so
-// barrier round trips between MMAs are paid serially; an A slot therefore
-// holds a whole 32-word pass (16 MMAs) per handshake, and the two converter
+// 64, two stacked layers 128.  The issuing warp blocks on each MMA, so an A
+// slot holds a whole pass (16 MMAs) per handshake, and the two converter
 // h-sets take alternate passes.
 //
-// Work decomposition: stream-K over units (128-row tile, 32-word K-chunk);
-// each CTA (one per SM, persistent) walks a contiguous unit range; each B chunk
-// staged in SMEM serves all k_used layers of the chunk.  A CTA that
-// covers a whole tile writes y directly; a CTA holding part of a tile parks
-// its int64 sums in its own slot and bumps the tile's arrival counter; the
-// last arriving CTA sums the slots of all contributors (fixed order, exact)
-// and resets the counter, so the workspace is left as it was found.
+// Work decomposition (TcPlan): units = (128-row tile, 1024-column K-chunk, all
+// k_used layers).  Default static schedule: CTA i of G = min(U, #SMs) owns units
+// [iU/G, (i+1)U/G); a segment (the CTA's units within one tile) that is a whole
+// tile is finalised from the CTA's own sums, a tile shared with a neighbouring
+// CTA is summed exactly with red.add.u64 and finalised by the contributor that
+// completes its chunk count (atom.acq_rel), which also re-zeroes the sums and
+// the counter, so the workspace is left as it was found.  PB_TC_STATIC=0 selects
+// dynamic claims with an end-of-work grid barrier instead.
 //
-// Warp roles (11 warps):
-//   warp 0      weight producer: TMA (cp.async.bulk.tensor.3d, 128B swizzle)
-//               of 128-row x 32-word bitlayer tiles into an 8-stage SMEM ring;
-//               starts before the activation kernel finishes (PDL);
-//   warp 1      TMEM allocator and MMA issuer (one elected lane);
-//   warp 2      B producer: 1-D bulk copies of the plane tiles (after PDL wait);
-//   warps 3..10 converters: thread = weight row; read the row's words of the
-//               pass's one or two tiles from the swizzled SMEM ring, build A,
-//               tcgen05.st it into the TMEM A ring (software-pipelined: a slot
-//               is published while the next is built); warps 3..6 also run
-//               the epilogue.
+// Warp roles (15 warps, 480 threads, one CTA per SM):
+//   warp 0       schedule + weight producer: TMA (cp.async.bulk.tensor.3d, 128B
+//                swizzle) of 128-row x 32-word tiles of the pair rows into a
+//                12-13-stage SMEM ring, from kernel start (before the PDL wait);
+//   warp 1       TMEM allocator and MMA issuer (one elected lane);
+//   warp 2       B producer: 1-D bulk copies of the plane tiles; the fused path's
+//                grid barrier that publishes the B slices;
+//   warps 3..10  converters (2 h-sets of 4): thread = weight row; read the pass's
+//                tiles from the swizzled ring, build A, tcgen05.st into the TMEM
+//                A ring (a slot is published while the next pass's tiles arrive);
+//   warps 11..14 fused prologue (a1-a2: max|x|, f_b, the B slice, the first
+//                chunk) and the epilogue (TMEM drain, Horner plane sums, exact
+//                int64 tile sums, dequant / bias / fn / LSTM cell / peer stores).
 #include <cuda.h>
 #include <cstdint>
 #include <cstdio>
@@ -931,7 +934,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     if (stored_pair) TWAIT(&bars.w_full[st1], (uint32_t)(((tc + 1) / p.wstages) & 1), 3);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[1] = gtimer();
                     publish();                          // previous pass's A is in TMEM: tell the MMA
-                    if (hold && pend_slot < 0 && (converted || p.dbg == 11)) {   // this h-set's first pass is published
+                    if (hold && pend_slot < 0 && converted) {   // this h-set's first pass is published
                         // fused path: after its first pass an h-set waits for the prologue (the
                         // epilogue warps' x wave and first B chunk), which it would otherwise
                         // slow down by competing for issue slots; the MMAs need both anyway
