@@ -166,3 +166,16 @@ def test_workspace_layout(pb):
     assert pb.pb_workspace_bytes(128, 4096, 16) >= 128 * 16 * 4096 // 8
     assert pb.pb_workspace_bytes(1, 10, 0) == 0
     assert pb.pb_rowshard_workspace_bytes(4, 1024, 16, 1000, 8) >= pb.pb_workspace_bytes(4, 1024, 16) + 4 * 4 * 125 * 9
+
+
+def test_p2p_argument_validation(pb):
+    # the fused peer all-gather's setup rejects bad arguments before any CUDA call
+    h = C.c_void_p()
+    hb = C.create_string_buffer(int(pb.pb_p2p_handle_bytes()) or 64)
+    assert pb.pb_p2p_create(C.byref(h), 3, 0, 1, 1024, hb) == pb.PB_EINVAL      # not 1, 2, 4 or 8 ranks
+    assert pb.pb_p2p_create(C.byref(h), 2, 2, 1, 1024, hb) == pb.PB_EINVAL      # rank out of range
+    assert pb.pb_p2p_create(C.byref(h), 16, 0, 1, 1024, hb) == pb.PB_EINVAL     # more than one node
+    assert pb.pb_p2p_create(C.byref(h), 2, 0, 0, 1024, hb) == pb.PB_EINVAL      # empty batch
+    assert pb.pb_p2p_open(None, hb) == pb.PB_EINVAL
+    assert pb.pb_matmul_rowshard_p2p(None, 1, None, 1024, 1, 16, pb.PB_ACT_AUTO, None, None, 0, None) == pb.PB_EINVAL
+    assert pb.pb_p2p_destroy(None) == pb.PB_OK
