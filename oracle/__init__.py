@@ -57,6 +57,7 @@ def lib():
         L.or_transpose.argtypes = [p, i64, i64, i32, p]
         L.or_bitserial.argtypes = [p, i64, i64, i32, i32, i32, dbl, p, p, p, i64, i32, p, p, i32]
         L.or_pbatch.argtypes = [p, i64, i64, i32, i32, dbl, i32, p, i64, i32, i32, p, p, p, i32]
+        L.or_pbatch_mid.argtypes = [p, i64, i64, i32, i32, dbl, i32, p, i64, i32, i32, p, p, p, i32, i32]
         L.or_search_clip.argtypes = [p, i64, i32, i32, p]
         L.or_lstm_cell.argtypes = [p, p, i64, i64, p, p]
         L.or_num_threads_available.restype = i32
@@ -162,7 +163,7 @@ def bitserial(layers, offset, k_used, scale, planes, xq, f, nthreads=1):
     return acc, y
 
 
-def pbatch(codes, L, offset, scale, k_used, x, a, act_frac=ACT_AUTO, nthreads=1):
+def pbatch(codes, L, offset, scale, k_used, x, a, act_frac=ACT_AUTO, nthreads=1, midpoint=False):
     """Whole Alg. 2 from integer codes [R][K] and float x [B][K].
 
     Returns (acc int64 [B][R], y float32 [B][R], f int32 [B])."""
@@ -174,8 +175,8 @@ def pbatch(codes, L, offset, scale, k_used, x, a, act_frac=ACT_AUTO, nthreads=1)
     acc = np.empty((B, R), np.int64)
     y = np.empty((B, R), np.float32)
     f = np.empty(B, np.int32)
-    st = lib().or_pbatch(_ptr(codes), R, K, L, offset, float(scale), k_used, _ptr(x), B, a,
-                         act_frac, _ptr(acc), _ptr(y), _ptr(f), nthreads)
+    st = lib().or_pbatch_mid(_ptr(codes), R, K, L, offset, float(scale), k_used, _ptr(x), B, a,
+                             act_frac, _ptr(acc), _ptr(y), _ptr(f), nthreads, 1 if midpoint else 0)
     if st != OK:
         raise ValueError(f"pbatch status {st}")
     return acc, y, f

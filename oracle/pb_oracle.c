@@ -272,14 +272,19 @@ int or_transpose(const int64_t* xq, int64_t B, int64_t K, int a, uint8_t* planes
  * layers [L][R][K], planes [B][a][K], xq [B][K] (for the offset term),
  * acc [B][R] (nullable), y [B][R] (nullable).  nthreads > 1 splits rows
  * (used only to time the oracle; integer results are order-independent).   */
-int or_bitserial(const uint8_t* layers, int64_t R, int64_t K, int L, int offset,
-                 int k_used, double scale, const uint8_t* planes,
-                 const int64_t* xq, const int32_t* f, int64_t B, int a,
-                 int64_t* acc, float* y, int nthreads)
+/* midpoint (an option the paper does not have): with k_used < L the
+ * kept layers represent the floor-truncated code m_trunc (reading G12); the midpoint
+ * option represents m_trunc + 2^(L - k_used - 1), the centre of the dropped range, so
+ * the product gains 2^(L - k_used - 1) * sum_c x_q[b, c].                             */
+int or_bitserial_mid(const uint8_t* layers, int64_t R, int64_t K, int L, int offset,
+                     int k_used, double scale, const uint8_t* planes,
+                     const int64_t* xq, const int32_t* f, int64_t B, int a,
+                     int64_t* acc, float* y, int nthreads, int midpoint)
 {
     if (!layers || !planes || !f || k_used < 1 || k_used > L || a < 1 || a > 32)
         return OR_EINVAL;
-    if (offset && !xq) return OR_EINVAL;
+    const int64_t mid = (midpoint && k_used < L && !offset) ? ((int64_t)1 << (L - k_used - 1)) : 0;
+    if ((offset || mid) && !xq) return OR_EINVAL;
     int bad = 0;
     if (nthreads < 1) nthreads = 1;
 #ifdef _OPENMP
@@ -304,6 +309,11 @@ int or_bitserial(const uint8_t* layers, int64_t R, int64_t K, int L, int offset,
                 for (int64_t c = 0; c < K; ++c) sx += xq[b * K + c];
                 total += (__int128)offset * sx;
             }
+            if (mid) {
+                __int128 sx = 0;
+                for (int64_t c = 0; c < K; ++c) sx += xq[b * K + c];
+                total += (__int128)mid * sx;
+            }
             if (total > (__int128)INT64_MAX || total < (__int128)INT64_MIN) { bad = 1; continue; }
             int64_t v = (int64_t)total;
             if (acc) acc[b * R + r] = v;
@@ -317,12 +327,22 @@ int or_bitserial(const uint8_t* layers, int64_t R, int64_t K, int L, int offset,
     return bad ? OR_ERANGE : OR_OK;
 }
 
+int or_bitserial(const uint8_t* layers, int64_t R, int64_t K, int L, int offset,
+                 int k_used, double scale, const uint8_t* planes,
+                 const int64_t* xq, const int32_t* f, int64_t B, int a,
+                 int64_t* acc, float* y, int nthreads)
+{
+    return or_bitserial_mid(layers, R, K, L, offset, k_used, scale, planes, xq, f, B, a, acc, y,
+                            nthreads, 0);
+}
+
 /* Whole Alg. 2 from integer codes: decompose -> cast -> transpose ->
  * bit-serial product -> reduce -> dequant.  Convenience composition of the
  * functions above, each step in the paper's order.                          */
-int or_pbatch(const int32_t* codes, int64_t R, int64_t K, int L, int offset,
-              double scale, int k_used, const float* x, int64_t B, int a,
-              int act_frac, int64_t* acc, float* y, int32_t* f_out, int nthreads)
+int or_pbatch_mid(const int32_t* codes, int64_t R, int64_t K, int L, int offset,
+                  double scale, int k_used, const float* x, int64_t B, int a,
+                  int act_frac, int64_t* acc, float* y, int32_t* f_out, int nthreads,
+                  int midpoint)
 {
     if (!codes || !x || R < 0 || K < 0 || B < 0) return OR_EINVAL;
     if (L < 1 || L > 16 || (offset && L != 1)) return OR_EINVAL;
@@ -347,12 +367,20 @@ int or_pbatch(const int32_t* codes, int64_t R, int64_t K, int L, int offset,
     if (st != OR_OK) goto done;
     st = or_transpose(xq, B, K, a, planes);
     if (st != OR_OK) goto done;
-    st = or_bitserial(layers, R, K, L, offset, k_used, scale, planes, xq, f, B, a,
-                      acc, y, nthreads);
+    st = or_bitserial_mid(layers, R, K, L, offset, k_used, scale, planes, xq, f, B, a,
+                          acc, y, nthreads, midpoint);
     if (f_out) for (int64_t b = 0; b < B; ++b) f_out[b] = f[b];
 done:
     free(layers); free(xq); free(planes); free(f);
     return st;
+}
+
+int or_pbatch(const int32_t* codes, int64_t R, int64_t K, int L, int offset,
+              double scale, int k_used, const float* x, int64_t B, int a,
+              int act_frac, int64_t* acc, float* y, int32_t* f_out, int nthreads)
+{
+    return or_pbatch_mid(codes, R, K, L, offset, scale, k_used, x, B, a, act_frac, acc, y,
+                         f_out, nthreads, 0);
 }
 
 /* Clip-threshold search ("optimize over a clipping threshold to find a

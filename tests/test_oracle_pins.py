@@ -327,3 +327,28 @@ def test_search_clip_property(orc):
         codes, s, _, _ = orc.quantize_weights(W, 5, "grid", clip)
         return np.mean(np.abs(s * codes - W))
     assert err(t) <= err(1.0)
+
+
+def test_midpoint_offset_identity_and_error(orc):
+    """SURVEY §8(f) f4 midpoint option (not in the paper): with k_used < L the kept layers
+    are the floor-truncated code (reading G12); the midpoint adds 2^(L-k_used-1) per code,
+    i.e. acc gains exactly 2^(L-k_used-1) * sum_c x_q -- and, being the centre of the
+    dropped range, lowers the error against the float product on Gaussian data."""
+    import numpy as np
+    import synth
+    R, K, L = 64, 512, 8
+    W = synth.weights(R, K, synth.seed(11, 0))
+    x = synth.activations(3, K, synth.seed(11, 1), "gauss")
+    codes, s, off, _ = orc.quantize_weights(W, L, "grid")
+    for k in (1, 3, 5, 7):
+        a0, y0, f = orc.pbatch(codes, L, off, s, k, x, 16)
+        a1, y1, _ = orc.pbatch(codes, L, off, s, k, x, 16, midpoint=True)
+        xq = np.trunc(np.ldexp(x.astype(np.float64), f[:, None])).astype(np.int64)   # exact cast (G8)
+        np.testing.assert_array_equal(a1 - a0, np.broadcast_to((1 << (L - k - 1)) * xq.sum(axis=1)[:, None], a0.shape))
+        ref = x.astype(np.float64) @ W.astype(np.float64).T
+        e0 = np.abs(y0 - ref).mean()
+        e1 = np.abs(y1 - ref).mean()
+        assert e1 < e0, (k, e0, e1)
+    a0, _, _ = orc.pbatch(codes, L, off, s, L, x, 16)
+    a1, _, _ = orc.pbatch(codes, L, off, s, L, x, 16, midpoint=True)
+    np.testing.assert_array_equal(a0, a1)          # k_used = L: nothing dropped, no offset
