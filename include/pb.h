@@ -208,6 +208,17 @@ pb_status pb_matmul(const float* x, int64_t batch, const pb_weights* w, int32_t 
                     int32_t act_bits, int32_t act_frac, float* y, int64_t* acc,
                     void* ws, size_t ws_bytes, pb_stream s);
 
+/* pb_matmul with options.  flags:
+ *   PB_MM_MIDPOINT  with k_used < L, represent each truncated code by the centre of
+ *                   its dropped range, m_trunc + 2^(L-k_used-1) (reading G12 gives the
+ *                   floor-truncated m_trunc; the midpoint is not in the paper): acc
+ *                   gains exactly 2^(L-k_used-1) * sum_c x_q[b,c].  No effect when
+ *                   k_used = L or for binary weights. */
+enum { PB_MM_MIDPOINT = 1 };
+pb_status pb_matmul_ex(const float* x, int64_t batch, const pb_weights* w, int32_t k_used,
+                       int32_t act_bits, int32_t act_frac, int32_t flags, float* y,
+                       int64_t* acc, void* ws, size_t ws_bytes, pb_stream s);
+
 /* FC layer helper: y = fn(W x + bias) (P:256 MNIST FC layers). */
 pb_status pb_linear(const float* x, int64_t batch, const pb_weights* w, int32_t k_used,
                     int32_t act_bits, int32_t act_frac, const float* bias, int32_t fn,

@@ -58,6 +58,7 @@ _SIGS = {
     "pb_bitgemm": ([_p, _sz, _i64, _W, _i32, _i32, _p, _p, _p, _i32, _i32, _p], _i32),
     "pb_matmul": ([_p, _i64, _W, _i32, _i32, _i32, _p, _p, _p, _sz, _p], _i32),
     "pb_linear": ([_p, _i64, _W, _i32, _i32, _i32, _p, _i32, _p, _p, _sz, _p], _i32),
+    "pb_matmul_ex": ([_p, _i64, _W, _i32, _i32, _i32, _i32, _p, _p, _p, _sz, _p], _i32),
     "pb_cell_workspace_bytes": ([_i64, _i64, _i64, _i32, _i32], _sz),
     "pb_rnn_step": ([_p, _p, _W, _W, _p, _p, _i32, _i32, _i32, _i64, _p, _p, _sz, _p], _i32),
     "pb_lstm_step": ([_p, _p, _p, _W, _W, _p, _p, _i32, _i32, _i32, _i64, _p, _p, _p, _sz, _p], _i32),
@@ -230,9 +231,13 @@ class Workspace:
         return self.buf.data_ptr()
 
 
+PB_MM_MIDPOINT = 1
+
+
 def matmul(x, w: PackedWeights, k_used=None, act_bits=16, act_frac=PB_ACT_AUTO, y=None, acc=None,
-           ws: Workspace | None = None, stream=None):
-    """y = W x (Alg. 2) for device float32 x [B][K]; returns y [B][R]."""
+           ws: Workspace | None = None, stream=None, midpoint=False):
+    """y = W x (Alg. 2) for device float32 x [B][K]; returns y [B][R].  midpoint: with
+    k_used < L, truncated codes stand for the centre of their dropped range (pb_matmul_ex)."""
     import torch
     B = x.shape[0]
     k_used = w.layers if k_used is None else k_used
@@ -240,8 +245,12 @@ def matmul(x, w: PackedWeights, k_used=None, act_bits=16, act_frac=PB_ACT_AUTO, 
         y = torch.empty((B, w.rows), dtype=torch.float32, device=x.device)
     if ws is None:
         ws = Workspace(workspace_bytes(B, w.cols, act_bits), x.device)
-    check(pb_matmul(_ptr(x), B, C.byref(w.desc), k_used, act_bits, act_frac, _ptr(y), _ptr(acc),
-                    ws.ptr, ws.nbytes, _stream(stream)))
+    if midpoint:
+        check(pb_matmul_ex(_ptr(x), B, C.byref(w.desc), k_used, act_bits, act_frac, PB_MM_MIDPOINT, _ptr(y),
+                           _ptr(acc), ws.ptr, ws.nbytes, _stream(stream)))
+    else:
+        check(pb_matmul(_ptr(x), B, C.byref(w.desc), k_used, act_bits, act_frac, _ptr(y), _ptr(acc),
+                        ws.ptr, ws.nbytes, _stream(stream)))
     return y
 
 

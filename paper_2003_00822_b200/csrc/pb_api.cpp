@@ -522,7 +522,7 @@ struct P2POut {
 static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
                           float* y, int64_t* acc, const float* bias, int32_t fn, int32_t accumulate, pb_stream s,
                           const float* x, int32_t act_frac, bool* fused_done, const CellOut* cell = nullptr,
-                          const P2POut* p2p = nullptr) {
+                          const P2POut* p2p = nullptr, bool midpoint = false) {
     if (fused_done) *fused_done = false;
 
     const pb::WsLayout l = pb::ws_layout(batch, w->kwords, act_bits);
@@ -546,6 +546,7 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     g.bias = bias;
     g.fn = fn;
     g.accumulate = accumulate ? 1 : 0;
+    g.mid = (midpoint && k_used < w->layers && !w->offset) ? (1ull << (w->layers - k_used - 1)) : 0ull;
     g.npad = pb::tc_npad(batch, act_bits);     // whole batch in one tensor-engine launch (else 0)
     g.bexp = reinterpret_cast<uint8_t*>(base + l.off_bexp);
     g.accbuf = reinterpret_cast<unsigned long long*>(base + l.off_slots);
@@ -662,23 +663,34 @@ pb_status pb_bitgemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_we
 // activation kernel followed by pb_bitgemm's engine.
 static pb_status act_and_gemm(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
                               int32_t act_frac, const float* bias, int32_t fn, float* y, int64_t* acc, void* ws,
-                              size_t ws_bytes, pb_stream s) {
+                              size_t ws_bytes, pb_stream s, bool midpoint = false) {
     pb_status st = validate_gemm(ws, ws_bytes, batch, w, k_used, act_bits, y, acc, fn);
     if (st != PB_OK) return st;
     if ((st = check_act(batch, w->cols, act_bits, act_frac)) != PB_OK) return st;
     if (batch == 0 || w->rows == 0) return PB_OK;
     if (!x || !aligned(x, 4)) return fail(PB_EINVAL, "x must be a non-NULL device pointer");
     bool fused = false;
-    st = run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, x, act_frac, &fused);
+    st = run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, x, act_frac, &fused, nullptr, nullptr,
+                  midpoint);
     if (fused || (st != PB_OK && st != PB_EINVAL)) return st;
     if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
-    return run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, nullptr, 0, nullptr);
+    return run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, nullptr, 0, nullptr, nullptr, nullptr,
+                    midpoint);
 }
 
 pb_status pb_matmul(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
                     int32_t act_frac, float* y, int64_t* acc, void* ws, size_t ws_bytes, pb_stream s) {
     g_err[0] = 0;
     return act_and_gemm(x, batch, w, k_used, act_bits, act_frac, nullptr, PB_FN_NONE, y, acc, ws, ws_bytes, s);
+}
+
+pb_status pb_matmul_ex(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
+                       int32_t act_frac, int32_t flags, float* y, int64_t* acc, void* ws, size_t ws_bytes,
+                       pb_stream s) {
+    g_err[0] = 0;
+    if (flags & ~PB_MM_MIDPOINT) return fail(PB_EINVAL, "unknown flags 0x%x", flags);
+    return act_and_gemm(x, batch, w, k_used, act_bits, act_frac, nullptr, PB_FN_NONE, y, acc, ws, ws_bytes, s,
+                        (flags & PB_MM_MIDPOINT) != 0);
 }
 
 pb_status pb_linear(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,

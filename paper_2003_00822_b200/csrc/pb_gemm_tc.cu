@@ -978,7 +978,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const int q = warp & 3;
         const int m = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0);
+        // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer; + the midpoint offset
+        const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0) + g.mid;
         bool have_xsum = false;
         auto xsum_of = [&](int b) -> unsigned long long {
             if (g.x) {

@@ -140,10 +140,10 @@ bitgemv_popc_kernel(const GemmArgs g)
 #pragma unroll
         for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
         if (lane == 0) {
-            if (g.offset) {
+            if (g.offset || g.mid) {           // binary offset and / or the midpoint offset
                 unsigned long long sx = 0;
                 for (int p = 0; p < g.nsplit; ++p) sx += (unsigned long long)g.xsum[(int64_t)b * kXsumStride + p];
-                tot += (unsigned long long)g.offset * sx;
+                tot += ((unsigned long long)g.offset + g.mid) * sx;
             }
             const long long accv = (long long)tot;
             const int64_t o = (int64_t)b * g.R + r;

@@ -101,6 +101,7 @@ struct GemmArgs {
     const float* bias;      // [R] or null
     int fn;
     int accumulate;
+    unsigned long long mid;       // midpoint offset 2^(L-k_used-1) (pb_matmul_ex PB_MM_MIDPOINT), else 0
     // tensor engine operands (valid when npad > 0)
     int npad;
     uint8_t* bexp;                // [kwords][npad x 32 canonical tile]

@@ -225,3 +225,25 @@ def test_tc_streamk_repeat(pb, torch, orc, R, K, B, L, k_used, a):
             compare(acc.cpu().numpy(), y.cpu().numpy(), acc_o, y_o)
     finally:
         pb.set_engine(pb.PB_ENGINE_AUTO)
+
+
+@pytest.mark.parametrize("engine", ["popc", "auto"])
+@pytest.mark.parametrize("R,K,B,L,k_used,a", [(1029, 784, 1, 4, 2, 16), (300, 4109, 3, 8, 5, 16),
+                                              (4096, 8192, 1, 8, 3, 16), (129, 1000, 2, 16, 9, 8),
+                                              (257, 1030, 1, 6, 6, 16)])
+def test_parity_midpoint(pb, torch, orc, engine, R, K, B, L, k_used, a):
+    # pb_matmul_ex(PB_MM_MIDPOINT) against the oracle's midpoint option
+    s = synth.seed(2, 7000 + R + K + L)
+    m = synth.codes(R, K, L, s)
+    x = synth.inject_edges(synth.activations(B, K, s + 1, "gauss"), s + 2)
+    w = pb.PackedWeights.from_codes(m, L, 0, 0.0123)
+    xd = torch.from_numpy(x).cuda()
+    acc = torch.zeros((B, R), dtype=torch.int64, device="cuda")
+    pb.set_engine(_engine(pb, engine))
+    try:
+        y = pb.matmul(xd, w, k_used, a, acc=acc, midpoint=True)
+    finally:
+        pb.set_engine(pb.PB_ENGINE_AUTO)
+    torch.cuda.synchronize()
+    acc_o, y_o, _ = orc.pbatch(m, L, 0, 0.0123, k_used, x, a, nthreads=8, midpoint=True)
+    compare(acc.cpu().numpy(), y.cpu().numpy(), acc_o, y_o)
