@@ -17,6 +17,7 @@ ap.add_argument("--a", type=int, default=16)
 ap.add_argument("--L", type=int, nargs="+", default=[1, 2, 4, 8, 16])
 ap.add_argument("--steps", type=int, default=64)
 ap.add_argument("--act-frac", type=int, default=-1024, help="PB_ACT_AUTO (-1024) or a literal f")
+ap.add_argument("--split", action="store_true", help="pb_act_quantize + pb_bitgemm instead of pb_matmul")
 ap.add_argument("--per", type=int, default=8, help="calls per CUDA graph (back to back, PDL-chained)")
 args = ap.parse_args()
 l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -41,10 +42,22 @@ for L in args.L:
     M = max(M, 2)
     while len(cp) < M:
         cp.append(w0.clone_to(torch.empty_like(w0.buf)))
+    def call(w):
+        if args.split:
+            pb.check(pb.pb_act_quantize(x.data_ptr(), args.B, args.K, args.a, args.act_frac, ws.ptr, ws.nbytes,
+                                        s.cuda_stream))
+            pb.check(pb.pb_bitgemm(ws.ptr, ws.nbytes, args.B, pb.C.byref(w.desc), L, args.a, y.data_ptr(), None,
+                                   None, 0, 0, s.cuda_stream))
+        else:
+            pb.matmul(x, w, L, args.a, args.act_frac, y=y, ws=ws, stream=s)
+    with torch.cuda.stream(s):
+        for w in cp:
+            call(w)
+    torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         for t in range(args.per):
-            pb.matmul(x, cp[t % M], L, args.a, args.act_frac, y=y, ws=ws, stream=s)
+            call(cp[t % M])
     reps = max(1, args.steps // args.per)
     for i in range(2):
         g.replay()
