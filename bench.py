@@ -9,13 +9,17 @@ batch 1 -- the largest configuration and the one the HBM-roofline target
 configs[0..3] are parity-test cases (tests/), not bench lines.
 
 One step = one pass of the whole hot path (plus a6
-all-gather when N > 1) over one synthetic input vector: pb_matmul (or
-pb_matmul_rowshard) through the C ABI, replayed from a CUDA graph.  Weights
-rotate over M packed copies whose total size is >= 2x L2, so every timed
-step streams its weights from HBM ("inputs larger than L2").
+all-gather when N > 1) over one synthetic input vector: pb_matmul (N > 1:
+pb_matmul_rowshard_p2p, the all-gather fused into the kernel over peer memory,
+verified against the NCCL pb_matmul_rowshard at start, NCCL as the fallback)
+through the C ABI, replayed from CUDA graphs of 8 back-to-back calls (exactly
+K timed steps).  Weights rotate over M >= 2 packed copies whose total size is
+>= 2x L2, so every timed step streams its weights from HBM ("inputs larger
+than L2").  Extras in the line: per-L / per-k_used sweeps, cuBLAS comparison
+systems, the LSTM-LM sequence (configs[2]) and the CPU oracle.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-  torchrun --nproc-per-node N bench.py --gpus N ...     (row-sharded, NCCL)
+  torchrun --nproc-per-node N bench.py --gpus N ...     (row-sharded)
 
 Prints ONE JSON line on rank 0.  See DESIGN.md "Measurement".
 """
