@@ -247,7 +247,7 @@ def main():
         if Lx == 1:
             assert N == 1, "binary sweep point is single-GPU"
             return pb.PackedWeights.quantize(Wl, 1, pb.PB_Q_BINARY)
-        return pb.PackedWeights.quantize_device(Wl_dev, Lx, step=pb.shard_grid_step(mn.item(), mx.item(), Lx))
+        return pb.PackedWeights.quantize_device(Wl_dev, Lx, step=pb.grid_step(mn.item(), mx.item(), Lx))
 
     def rotation(w):
         nb = w.nbytes()

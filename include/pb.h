@@ -124,6 +124,14 @@ pb_status pb_quantize_pack_weights_step(const float* W_host, int64_t rows, int64
                                         int32_t layers, double step, void* dst,
                                         int32_t dst_is_device, pb_stream s, pb_weights* out);
 
+/* The Q(W) grid step of P:149, d = (w_max - w_min) / 2^(L-1) for L = layers stored
+ * bitlayers (reading G1), from given extrema -- e.g. the min/max all-reduced over the
+ * row shards of one layer, so every rank packs with the unsharded layer's grid.
+ * Degenerate extrema (w_max == w_min, reading G5): *step = |w_max|, or 1 when both are 0,
+ * and PB_EDEGENERATE is returned (the step is still written).  PB_EINVAL for a NULL
+ * step, layers outside [2,16], non-finite extrema or w_min > w_max.  Host only. */
+pb_status pb_grid_step(double w_min, double w_max, int32_t layers, double* step);
+
 /* Step a0 on the GPU, for a float32 W [rows][cols] already
  * in device memory: the PB_Q_GRID quantiser (readings G4, G5) and
  * the bitlayer packer, producing exactly the bytes and scale of
@@ -165,8 +173,9 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
  *                                             zero on entry, left zero
  *   [f_b int32 x batch][x_q partial sums int64 x batch x 160]
  *   [planes uint32 x batch x act_bits x kwords]
- *   [tensor-engine B operand tiles: kwords x N_pad x 32 bytes, N_pad = a*batch
- *    padded to 8/16/32, present when a*batch <= 32]
+ *   [tensor-engine B operand tiles of one launch's batch slice: roundup(kwords, 32)
+ *    x N_pad x 16 bytes, N_pad = a * slice padded to 8/16/32/64; slice = batch
+ *    when a*batch <= 64 and batch <= 32, else min(32, 64/a) columns]
  * each region 256-byte aligned.  The workspace must be zero-filled before its
  * first use (the counters); every other region is rewritten by each call, so
  * one workspace serves calls of any shape with the same act_bits (the
@@ -264,7 +273,10 @@ pb_status pb_lstm_step(const float* x_t, const float* h, const float* c,
  *   c_seq  device [steps][batch][H] or NULL: c_1 .. c_steps;
  *   c_last device [batch][H]: c_steps (required).
  * Stream-ordered, graph-capturable, no allocation.  PB_EINVAL: shapes, NULLs,
- * workspace < pb_lstm_seq_workspace_bytes. */
+ * k_used outside [1, L] of either matrix, steps*batch > 65535 (the hoisted
+ * projection is one batched call), workspace < pb_lstm_seq_workspace_bytes;
+ * PB_ERANGE: the reading-G11 accumulator bound of either matrix.  Every check
+ * runs before the first launch. */
 size_t pb_lstm_seq_workspace_bytes(int64_t steps, int64_t batch, int64_t in_cols,
                                    int64_t hidden, int32_t act_bits);
 pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float* h0,

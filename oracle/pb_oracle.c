@@ -29,8 +29,10 @@
  * Parity pins (tests/test_oracle_pins.py): the Supplement §1 worked example
  * (P:386-467), exhaustive two's-complement identity, brute-force
  * integer matmul of the quantised values, the binary special case, k_used
- * truncation, Q(W) closed forms, the activation cast, convergence to float.
- * parity unpinned: or_search_clip (G6: the paper fixes no candidate set).
+ * truncation, Q(W) closed forms, the activation cast, convergence to float,
+ * or_lstm_cell against PyTorch's nn.LSTMCell in float64 (reading G15).
+ * parity unpinned: or_search_clip (G6: the paper fixes no candidate set; it
+ * is checked only for the property "never worse than no clip").
  */
 #include <math.h>
 #include <stdint.h>
@@ -413,7 +415,8 @@ int or_search_clip(const float* W, int64_t n_el, int L, int ncand, float* clip_o
 
 /* Elementwise LSTM / RNN cells in double (reading G15: PyTorch nn.LSTM gate
  * order i, f, g, o; RNN cell = tanh).  gates [B][4H] (pre-activation, the
- * sum of the two quantised matvecs plus biases).                            */
+ * sum of the two quantised matvecs plus biases).  Pinned to torch.nn.LSTMCell
+ * (tests/test_oracle_pins.py::test_lstm_cell_matches_torch_lstmcell).       */
 static double or_sigmoid(double v) { return 1.0 / (1.0 + exp(-v)); }
 
 int or_lstm_cell(const double* gates, const float* c, int64_t B, int64_t H,

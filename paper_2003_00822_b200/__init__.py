@@ -49,6 +49,7 @@ _SIGS = {
     "pb_packed_bytes": ([_i64, _i64, _i32], _sz),
     "pb_quantize_pack_weights": ([_p, _i64, _i64, _i32, _i32, _f32, _p, _i32, _p, _W], _i32),
     "pb_quantize_pack_weights_step": ([_p, _i64, _i64, _i32, _dbl, _p, _i32, _p, _W], _i32),
+    "pb_grid_step": ([_dbl, _dbl, _i32, C.POINTER(_dbl)], _i32),
     "pb_pack_codes": ([_p, _i64, _i64, _i32, _i32, _dbl, _p, _i32, _p, _W], _i32),
     "pb_pack_device_workspace_bytes": ([], _sz),
     "pb_quantize_pack_weights_device": ([_p, _i64, _i64, _i32, _f32, _dbl, _p, _p, _sz, _p, _W], _i32),
@@ -452,13 +453,12 @@ def shard_codes(codes, nranks, rank, offset=0):
     return out
 
 
-def shard_grid_step(W_min, W_max, L):
-    """Global Q(W) grid step d = (max - min) / 2^(L-1) from the
-    all-reduced extrema of the shards, for PackedWeights.quantize_step."""
-    d = (float(W_max) - float(W_min)) / float(2 ** (L - 1))
-    if d == 0.0:
-        d = abs(float(W_max)) or 1.0
-    return d
+def grid_step(W_min, W_max, L):
+    """pb_grid_step: the Q(W) grid step of the layer with these extrema (e.g. the
+    all-reduced min/max of its row shards), for PackedWeights.quantize_step."""
+    d = C.c_double()
+    check(pb_grid_step(float(W_min), float(W_max), L, C.byref(d)), (PB_OK, PB_EDEGENERATE))
+    return d.value
 
 
 def debug_timeline(max_records=1 << 16):

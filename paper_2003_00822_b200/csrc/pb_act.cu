@@ -83,10 +83,15 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
     if (blockIdx.x == 0 && tid == 0) f_out[b] = f;
 
     // ---- a1 (part 2) + a2: cast, saturate, ballot-transpose ----
-    const int64_t w0 = (int64_t)blockIdx.x * words_per_cta;
+    int64_t w0 = (int64_t)blockIdx.x * words_per_cta;
     int64_t w1 = w0 + words_per_cta;
     if (w1 > kwords) w1 = kwords;
-    if (npad && blockIdx.x == gridDim.x - 1) w1 = (kwords + 31) / 32 * 32;   // zero B for the chunk tail
+    if (npad && blockIdx.x == gridDim.x - 1) {
+        // zero B for the chunk tail [kwords, roundup(kwords, 32)); with a capped split the
+        // last CTA's own range may start beyond kwords, so it starts at min(w0, kwords)
+        if (w0 > kwords) w0 = kwords;
+        w1 = (kwords + 31) / 32 * 32;
+    }
     uint32_t* pb = planes + (int64_t)b * a * kwords;
     long long xs = 0;
     for (int64_t w = w0 + warp; w < w1; w += kWarps) {

@@ -390,6 +390,21 @@ pb_status pb_quantize_pack_weights_device(const float* W_dev, int64_t rows, int6
     return PB_OK;
 }
 
+pb_status pb_grid_step(double w_min, double w_max, int32_t layers, double* step) {
+    g_err[0] = 0;
+    if (!step) return fail(PB_EINVAL, "step is NULL");
+    if (layers < 2 || layers > 16) return fail(PB_EINVAL, "layers=%d not in [2,16]", layers);
+    if (!std::isfinite(w_min) || !std::isfinite(w_max) || w_min > w_max)
+        return fail(PB_EINVAL, "extrema must be finite with min <= max");
+    bool deg = false;
+    *step = grid_step(w_min, w_max, layers - 1, deg);
+    if (deg) {
+        fail(PB_EDEGENERATE, "max(W) == min(W): degenerate grid (reading G5)");
+        return PB_EDEGENERATE;
+    }
+    return PB_OK;
+}
+
 pb_status pb_quantize_pack_weights_step(const float* W_host, int64_t rows, int64_t cols, int32_t layers,
                                         double step, void* dst, int32_t dst_is_device, pb_stream s,
                                         pb_weights* out) {
@@ -482,6 +497,20 @@ pb_status pb_act_quantize(const float* x, int64_t batch, int64_t cols, int32_t a
     return PB_OK;
 }
 
+// One matvec's knobs: the descriptor, k_used in [1, L] (reading G12) and the int64
+// accumulator bound of reading G11, |acc| <= K 2^(L-1) 2^(a-1) (+ K 2^(a-1) for the offset)
+// < 2^63.  Checked before any launch by every entry point that runs the matvec.
+static pb_status check_matvec(const pb_weights* w, int32_t k_used, int32_t act_bits, const char* what) {
+    pb_status st = check_weights(w);
+    if (st != PB_OK) return st;
+    if (k_used < 1 || k_used > w->layers)
+        return fail(PB_EINVAL, "%s: k_used=%d not in [1,%d]", what, k_used, w->layers);
+    if (act_bits < 1 || act_bits > 32) return fail(PB_EINVAL, "act_bits=%d not in [1,32]", act_bits);
+    const int bound = ceil_log2(w->cols > 1 ? w->cols : 1) + w->layers + act_bits - 2 + (w->offset ? 1 : 0);
+    if (bound > 62) return fail(PB_ERANGE, "%s: accumulator bound 2^%d exceeds int64 (reading G11)", what, bound + 1);
+    return PB_OK;
+}
+
 static pb_status validate_gemm(const void* ws, size_t ws_bytes, int64_t batch, const pb_weights* w,
                                int32_t k_used, int32_t act_bits, const float* y, const int64_t* acc,
                                int32_t fn) {
@@ -489,13 +518,10 @@ static pb_status validate_gemm(const void* ws, size_t ws_bytes, int64_t batch, c
     if (st != PB_OK) return st;
     if ((st = check_act(batch, w->cols, act_bits, PB_ACT_AUTO)) != PB_OK) return st;
     if ((st = check_ws(ws, ws_bytes, batch, w->cols, act_bits)) != PB_OK) return st;
-    if (k_used < 1 || k_used > w->layers) return fail(PB_EINVAL, "k_used=%d not in [1,%d]", k_used, w->layers);
+    if ((st = check_matvec(w, k_used, act_bits, "W")) != PB_OK) return st;
     if (fn < PB_FN_NONE || fn > PB_FN_SIGMOID) return fail(PB_EINVAL, "fn=%d unknown", fn);
     if (batch * w->rows > 0 && (!y || !aligned(y, 4))) return fail(PB_EINVAL, "y must be a non-NULL device pointer");
     if (acc && !aligned(acc, 8)) return fail(PB_EINVAL, "acc must be 8-byte aligned");
-    // reading G11: |acc| <= K 2^(L-1) 2^(a-1) (+ K 2^(a-1) for the offset) < 2^63
-    const int bound = ceil_log2(w->cols > 1 ? w->cols : 1) + w->layers + act_bits - 2 + (w->offset ? 1 : 0);
-    if (bound > 62) return fail(PB_ERANGE, "accumulator bound 2^%d exceeds int64 (reading G11)", bound + 1);
     return PB_OK;
 }
 
@@ -744,15 +770,18 @@ size_t pb_cell_workspace_bytes(int64_t batch, int64_t in_cols, int64_t hidden, i
 
 static pb_status cell_common(const float* x_t, const float* h, const pb_weights* w_ih, const pb_weights* w_hh,
                              const float* b_ih, const float* b_hh, int32_t k_ih, int32_t k_hh, int32_t a,
-                             int64_t batch, int gates, void* ws, size_t ws_bytes, pb_stream s, float** gbuf) {
+                             int64_t batch, int gates, void* ws, size_t ws_bytes, pb_stream s, float** gbuf,
+                             bool outs_ok) {
     pb_status st;
-    if ((st = check_weights(w_ih)) != PB_OK) return st;
-    if ((st = check_weights(w_hh)) != PB_OK) return st;
+    if ((st = check_matvec(w_ih, k_ih, a, "W_ih")) != PB_OK) return st;
+    if ((st = check_matvec(w_hh, k_hh, a, "W_hh")) != PB_OK) return st;
     const int64_t H = w_hh->cols;
     if (w_ih->rows != gates * H || w_hh->rows != gates * H)
         return fail(PB_EINVAL, "W_ih/W_hh must have %d*H rows (H = W_hh cols = %lld)", gates, (long long)H);
+    if ((st = check_act(batch, w_ih->cols > H ? w_ih->cols : H, a, PB_ACT_AUTO)) != PB_OK) return st;
     const size_t need = pb_cell_workspace_bytes(batch, w_ih->cols, H, a, gates);
     if (!ws || !aligned(ws, 16) || ws_bytes < need) return fail(PB_EINVAL, "cell workspace %zu < %zu", ws_bytes, need);
+    if (!outs_ok) return fail(PB_EINVAL, "x/h and the outputs (h_out, and c/c_out for the LSTM) must be non-NULL");
     const int64_t k = w_ih->cols > H ? w_ih->cols : H;
     const size_t act_ws = pb::align_up(pb_workspace_bytes(batch, k, a));
     *gbuf = reinterpret_cast<float*>(static_cast<char*>(ws) + act_ws);
@@ -768,10 +797,10 @@ pb_status pb_rnn_step(const float* x_t, const float* h, const pb_weights* w_ih, 
                       int64_t batch, float* h_out, void* ws, size_t ws_bytes, pb_stream s) {
     g_err[0] = 0;
     float* gates = nullptr;
+    const bool outs = batch == 0 || (x_t && h && h_out);
     pb_status st = cell_common(x_t, h, w_ih, w_hh, b_ih, b_hh, k_used_ih, k_used_hh, act_bits, batch, 1, ws,
-                               ws_bytes, s, &gates);
+                               ws_bytes, s, &gates, outs);
     if (st != PB_OK) return st;
-    if (!h_out) return fail(PB_EINVAL, "h_out is NULL");
     cudaError_t e = pb::launch_rnn_cell(gates, batch, w_hh->cols, h_out, static_cast<cudaStream_t>(s));
     if (e != cudaSuccess) return cuda_fail(e, "rnn_cell launch");
     return PB_OK;
@@ -783,10 +812,10 @@ pb_status pb_lstm_step(const float* x_t, const float* h, const float* c, const p
                        size_t ws_bytes, pb_stream s) {
     g_err[0] = 0;
     float* gates = nullptr;
+    const bool outs = batch == 0 || (x_t && h && c && h_out && c_out);
     pb_status st = cell_common(x_t, h, w_ih, w_hh, b_ih, b_hh, k_used_ih, k_used_hh, act_bits, batch, 4, ws,
-                               ws_bytes, s, &gates);
+                               ws_bytes, s, &gates, outs);
     if (st != PB_OK) return st;
-    if (!h_out || !c_out || !c) return fail(PB_EINVAL, "c/h_out/c_out is NULL");
     cudaError_t e = pb::launch_lstm_cell(gates, c, batch, w_hh->cols, h_out, c_out, static_cast<cudaStream_t>(s));
     if (e != cudaSuccess) return cuda_fail(e, "lstm_cell launch");
     return PB_OK;
@@ -808,12 +837,15 @@ pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float*
                       size_t ws_bytes, pb_stream s) {
     g_err[0] = 0;
     pb_status st;
-    if ((st = check_weights(w_ih)) != PB_OK) return st;
-    if ((st = check_weights(w_hh)) != PB_OK) return st;
+    if ((st = check_matvec(w_ih, k_used_ih, act_bits, "W_ih")) != PB_OK) return st;
+    if ((st = check_matvec(w_hh, k_used_hh, act_bits, "W_hh")) != PB_OK) return st;
     const int64_t H = w_hh->cols, E = w_ih->cols;
     if (w_ih->rows != 4 * H || w_hh->rows != 4 * H)
         return fail(PB_EINVAL, "W_ih/W_hh must have 4*H rows (H = W_hh cols = %lld)", (long long)H);
     if (steps < 0 || batch < 0) return fail(PB_EINVAL, "steps/batch < 0");
+    if (steps * batch > 65535)
+        return fail(PB_EINVAL, "steps*batch=%lld > 65535 (the hoisted input projection is one batched call)",
+                    (long long)(steps * batch));
     if (steps == 0 || batch == 0 || H == 0) return PB_OK;
     if (!x || !h0 || !c0 || !h_seq || !c_last) return fail(PB_EINVAL, "x/h0/c0/h_seq/c_last is NULL");
     const size_t need = pb_lstm_seq_workspace_bytes(steps, batch, E, H, act_bits);

@@ -59,6 +59,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <mutex>
 
 #include "pb_common.cuh"
 #include "pb_internal.h"
@@ -1056,6 +1057,12 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                                  "l"(kGridStride / (unsigned)g.nranks)
                                  : "memory");
         }
+        if (g.nranks && p.stat) {
+            // the static schedule finalises (and stores into every rank's y_full) from its first
+            // segment on: wait until every rank has entered this call before any remote store
+            if (ew == 0 && lane == 0) sys_wait(g.local_ctr + 1, rbase + kGridStride);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
         int seg = 0;
         while (true) {
             const int2 it = take_item(bars, qi, qph, lane);
@@ -1190,7 +1197,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             grid_arrive(g.ebar);
             grid_wait(g.ebar, ebase);                // acquire; bar.sync passes it to the CTA
             if (g.nranks)                            // every rank has entered this call (f2)
-                sys_wait(g.local_ctr + 1, rbase + kGridStride);
+                sys_wait(g.local_ctr + 1, rbase + kGridStride);   // (the static schedule waited above)
             if TLP(g) bars.t_ebar[1] = gtimer();
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -1332,16 +1339,62 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     return true;
 }
 
+// Per-device launch state: SM count and whether the kernel's attributes are set (function
+// attributes belong to the device's context, so one process driving several GPUs sets them on
+// each).  Devices are few; the table is written once per (device, NPAD) under a mutex.
+struct DevState {
+    int sms = 0;
+    bool attr[4] = {false, false, false, false};
+};
+constexpr int kMaxDevices = 64;
+DevState g_dev[kMaxDevices];
+std::mutex g_dev_mu;
+
+// Tensor maps of recently used weight buffers (per thread, tiny LRU): encoding two
+// CUtensorMaps costs a few microseconds of host time per un-graphed call otherwise.
+struct MapEntry {
+    const uint32_t* bits = nullptr;
+    int64_t R = 0, kwords = 0;
+    int L = 0, dev = -1;
+    CUtensorMap pmap, smap;
+    unsigned long long used = 0;
+};
+constexpr int kMapCache = 8;
+thread_local MapEntry t_maps[kMapCache];
+thread_local unsigned long long t_map_clock = 0;
+
+cudaError_t weight_maps_cached(const GemmArgs& g, int dev, CUtensorMap* pmap, CUtensorMap* smap)
+{
+    MapEntry* victim = &t_maps[0];
+    for (int i = 0; i < kMapCache; ++i) {
+        MapEntry& e = t_maps[i];
+        if (e.bits == g.bits && e.R == g.R && e.kwords == g.kwords && e.L == g.L && e.dev == dev) {
+            e.used = ++t_map_clock;
+            *pmap = e.pmap;
+            *smap = e.smap;
+            return cudaSuccess;
+        }
+        if (e.used < victim->used) victim = &e;
+    }
+    cudaError_t r = make_weight_maps(g, pmap, smap);
+    if (r != cudaSuccess) return r;
+    victim->bits = g.bits;
+    victim->R = g.R;
+    victim->kwords = g.kwords;
+    victim->L = g.L;
+    victim->dev = dev;
+    victim->pmap = *pmap;
+    victim->smap = *smap;
+    victim->used = ++t_map_clock;
+    return cudaSuccess;
+}
+
 template <int NPAD>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 {
-    static int sms = 0;
-    static bool attr = false;
     static int dbg = -1, prof = 0, bst_env = 0, stat_env = -1, dyn_pct = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static std::once_flag env_once;
+    std::call_once(env_once, [] {
         const char* ev = getenv("PB_TC_DEBUG");
         dbg = ev ? atoi(ev) : 0;
         ev = getenv("PB_TC_PROF");
@@ -1352,15 +1405,30 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
         stat_env = ev ? atoi(ev) : -1;
         ev = getenv("PB_TC_DYN");              // experiment knob: % of units claimed dynamically
         dyn_pct = ev ? atoi(ev) : 0;
+    });
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    DevState& ds = g_dev[dev];
+    constexpr int ai = NPAD == 8 ? 0 : (NPAD == 16 ? 1 : (NPAD == 32 ? 2 : 3));
+    if (!ds.attr[ai] || !ds.sms) {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        if (!ds.sms) {
+            int n = 0;
+            if ((e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+            ds.sms = n;
+        }
+        if (!ds.attr[ai]) {
+            e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemMax);
+            if (e != cudaSuccess) return e;
+            cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared);
+            ds.attr[ai] = true;
+        }
     }
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kSmemMax);
-        if (e != cudaSuccess) return e;
-        cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             (int)cudaSharedmemCarveoutMaxShared);
-        attr = true;
-    }
+    const int sms = ds.sms;
     TcPlan p;
     if (!make_plan(g, NPAD, p)) return cudaErrorNotSupported;
     if (stat_env != 0) {                       // default: static (PB_TC_STATIC=0: dynamic claims)
@@ -1375,7 +1443,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
         p.items = p.gs + (p.units - p.ustat);
     }
     CUtensorMap pmap, smap;
-    cudaError_t e = make_weight_maps(g, &pmap, &smap);
+    e = weight_maps_cached(g, dev, &pmap, &smap);
     if (e != cudaSuccess) return e;
     p.dbg = dbg;
     p.prof = prof;

@@ -17,7 +17,7 @@ constexpr int kMaxRanks = 8;         // pb_matmul_rowshard_p2p: ranks of one nod
 
 inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
 
-// MMA N (plane columns a*batch padded to a legal tcgen05 kind::i8 N for M = 128),
+// MMA N (plane columns a*batch padded to a legal tcgen05 kind::mxf4 N for M = 128),
 // 0 when the tensor engine's operand tiles are not produced for this shape.
 inline int tc_npad(int64_t batch, int32_t a) {
     const int64_t n = batch * a;
@@ -36,12 +36,12 @@ inline int64_t tc_slice(int64_t batch, int32_t a) {
 // Workspace carve-up (documented in pb.h, pb_workspace_bytes):
 //   [tile counters int32 x kMaxTiles]   stream-K arrival counters; zero on
 //                                       entry, every call leaves them zero
-//   [grid barrier int32 x 2]            fused tensor-engine path: arrival
-//                                       count (left zero) + generation
+//   [grid barrier uint64]               fused tensor-engine path: monotonic
+//                                       arrival counter (+2^20 per call)
 //   [work counters int32 x 2]           tensor engine: item claims, finished
 //                                       CTAs (left zero)
-//   [end barrier int32 x 2]             tensor engine: arrival count (left
-//                                       zero) + generation
+//   [end barrier uint64]                tensor engine (dynamic schedule):
+//                                       monotonic arrival counter
 //   [tile sums int64 x kAccTiles x B x 128]   tensor engine: partial-tile
 //                                       accumulators (left zero)
 //   [f_b int32 x B][Σx_q partials int64 x B x kXsumStride][bit planes [B][a][kwords]]
@@ -113,9 +113,9 @@ struct GemmArgs {
     const float* x;               // [B][K] or null
     int64_t K;
     int act_frac;
-    int* gbar;                    // grid barrier {arrival count, generation}
+    int* gbar;                    // grid barrier: monotonic uint64 arrival counter (+2^20 per call)
     int* work;                    // tensor engine {item claim counter, finished CTAs}, zero between calls
-    int* ebar;                    // tensor engine end-of-work grid barrier {arrival count, generation}
+    int* ebar;                    // end-of-work grid barrier (dynamic schedule), monotonic uint64
     // fused LSTM cell (pb_lstm_seq, tensor engine): rows are gate-interleaved (row 4k + gate,
     // gates i, f, g, o); the finalisation applies the cell to the four pre-activations of
     // hidden unit k (dequant + bias + y when accumulate) and writes h, c instead of y

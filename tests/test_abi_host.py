@@ -90,6 +90,26 @@ def test_packer_clip_and_degenerate(pb, orc):
     assert st == pb.PB_EDEGENERATE and d.scale == 1.0 and not buf.any()
 
 
+@pytest.mark.parametrize("L", [2, 3, 8, 16])
+def test_grid_step_matches_oracle(pb, orc, L):
+    # pb_grid_step from a layer's extrema == the oracle quantiser's d on the whole layer,
+    # also when the extrema are all-reduced over row shards (the max/min of the shards' extrema)
+    W = synth.weights(37, 300, synth.seed(1, L), "student_t")
+    _, d_or, _ = orc.quantize_round(W, L - 1)
+    shards = np.array_split(W, 3)
+    mn = min(float(s.min()) for s in shards)
+    mx = max(float(s.max()) for s in shards)
+    assert pb.grid_step(mn, mx, L) == d_or
+    # reading G5: constant W -> |c| (PB_EDEGENERATE), all-zero -> 1; bad arguments
+    d = C.c_double()
+    assert pb.pb_grid_step(-0.25, -0.25, L, C.byref(d)) == pb.PB_EDEGENERATE and d.value == 0.25
+    assert orc.quantize_round(np.full((2, 3), -0.25, np.float32), L - 1)[1] == 0.25
+    assert pb.pb_grid_step(0.0, 0.0, L, C.byref(d)) == pb.PB_EDEGENERATE and d.value == 1.0
+    assert pb.pb_grid_step(1.0, 0.0, L, C.byref(d)) == pb.PB_EINVAL
+    assert pb.pb_grid_step(0.0, 1.0, 1, C.byref(d)) == pb.PB_EINVAL
+    assert pb.pb_grid_step(0.0, float("inf"), L, C.byref(d)) == pb.PB_EINVAL
+
+
 def test_pack_codes_and_range(pb, orc):
     m = synth.codes(4, 77, 6, 9)
     buf = np.zeros(pb.pb_packed_bytes(4, 77, 6) // 4, np.uint32)

@@ -352,3 +352,34 @@ def test_midpoint_offset_identity_and_error(orc):
     a0, _, _ = orc.pbatch(codes, L, off, s, L, x, 16)
     a1, _, _ = orc.pbatch(codes, L, off, s, L, x, 16, midpoint=True)
     np.testing.assert_array_equal(a0, a1)          # k_used = L: nothing dropped, no offset
+
+
+# ----------------------------------------------------------------- P9 (reading G15)
+def test_lstm_cell_matches_torch_lstmcell(orc):
+    # or_lstm_cell is pinned to PyTorch's nn.LSTMCell (reading G15: PyTorch nn.LSTM semantics,
+    # gate order i, f, g, o; P:258 LSTM LM).  nn.LSTMCell computes its gates as
+    # W_ih x + b_ih + W_hh h + b_hh; with W_ih = I (4H x 4H), W_hh = 0 and zero biases the gate
+    # pre-activations are exactly x, so LSTMCell(x = gates, (h, c)) is the cell alone, in float64.
+    # A swapped gate (e.g. i <-> f, or tanh on o) or a wrong update (c' = i c + f g) fails here.
+    import torch
+    B, H = 5, 37
+    rng = np.random.default_rng(20200302)
+    gates = rng.normal(0.0, 2.0, (B, 4 * H))
+    gates[0, :] = 0.0                                     # sigmoid(0) = 1/2, tanh(0) = 0
+    gates[1, :H] = 30.0                                   # saturated input gate
+    c = rng.normal(0.0, 1.0, (B, H)).astype(np.float32)
+    cell = torch.nn.LSTMCell(4 * H, H, bias=True, dtype=torch.float64)
+    with torch.no_grad():
+        cell.weight_ih.copy_(torch.eye(4 * H, dtype=torch.float64))
+        cell.weight_hh.zero_()
+        cell.bias_ih.zero_()
+        cell.bias_hh.zero_()
+        h_t, c_t = cell(torch.from_numpy(gates), (torch.zeros(B, H, dtype=torch.float64),
+                                                   torch.from_numpy(c.astype(np.float64))))
+    h_o, c_o = orc.lstm_cell(gates, c)
+    np.testing.assert_allclose(c_o, c_t.numpy(), rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(h_o, h_t.numpy(), rtol=1e-13, atol=1e-15)
+    # closed form at zero gates: c' = c / 2, h' = tanh(c / 2) / 2
+    c0 = c[0].astype(np.float64)
+    np.testing.assert_allclose(c_o[0], c0 / 2.0, rtol=1e-15)
+    np.testing.assert_allclose(h_o[0], np.tanh(c0 / 2.0) / 2.0, rtol=1e-14)

@@ -41,7 +41,7 @@ def _worker(rank, world, port, R, K, L, B, a, q):
         mx = torch.tensor([float(Wl[:nr].max()) if nr else -np.inf], dtype=torch.float64)
         dist.all_reduce(mn, dist.ReduceOp.MIN)
         dist.all_reduce(mx, dist.ReduceOp.MAX)
-        step = pb.shard_grid_step(mn.item(), mx.item(), L)
+        step = pb.grid_step(mn.item(), mx.item(), L)
         # host pack of the shard with the global step
         buf = np.zeros(pb.pb_packed_bytes(rs, K, L) // 4, np.uint32)
         d = pb.pb_weights()
