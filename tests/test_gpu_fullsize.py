@@ -86,4 +86,4 @@ def test_c3_lstm_gate_matvec(pb, torch, orc):
 
 def test_c4_nli_batch128(pb, torch, orc):
     # configs[3]: 16384 x 4096, batch 128 (batched bitlayer GEMM regime)
-    _check(pb, torch, orc, 16384, 4096, 8, 16, 128, 8, "gauss", 4, rows_sample=6)
+    _check(pb, torch, orc, 16384, 4096, 8, 16, 128, 8, "gauss", 4, rows_sample=64)

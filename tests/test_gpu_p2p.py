@@ -4,8 +4,10 @@ small enough that all ranks' CTAs are resident together, and the ranks' buffers 
 joined with pb_p2p_open_peers.  The kernel's remote y stores, the cross-rank arrival
 counters (red.release.sys / ld.acquire.sys) and the entry handshake run as they do
 across NVLink; only the IPC mapping differs (pb_p2p_open, used by bench.py under
-torchrun).  Every rank's y_full must equal pb_matmul on the whole layer bit-exactly,
-over repeated calls (monotonic counters) and inside CUDA graphs."""
+torchrun).  Every rank's y_full must equal the oracle's y on the whole layer (identical
+bits, reading G13) -- and pb_matmul's -- over repeated calls (monotonic counters), inside
+CUDA graphs, and over back-to-back calls with changing x and no host sync between them
+(a fast rank must not overwrite a peer's y_full while the peer still reads it)."""
 import numpy as np
 import pytest
 
@@ -24,7 +26,7 @@ def pb():
 
 @pytest.mark.parametrize("N,R,K,L,B", [(2, 2048, 2048, 4, 1), (2, 1000, 784, 3, 3), (2, 4096, 4096, 8, 2),
                                        (4, 2048, 1024, 5, 1), (8, 1030, 512, 2, 2), (2, 2048, 2048, 16, 4)])
-def test_p2p_ranks_on_one_gpu(pb, N, R, K, L, B):
+def test_p2p_ranks_on_one_gpu(pb, orc, N, R, K, L, B):
     import torch
     m = synth.codes(R, K, L, 5 + N)
     w_full = pb.PackedWeights.from_codes(m, L, 0, 0.25)
@@ -34,8 +36,11 @@ def test_p2p_ranks_on_one_gpu(pb, N, R, K, L, B):
     streams = [torch.cuda.Stream() for _ in range(N)]
     try:
         for it in range(3):
-            x = torch.from_numpy(synth.activations(B, K, 6 + it)).cuda()
+            xh = synth.activations(B, K, 6 + it)
+            x = torch.from_numpy(xh).cuda()
             ref = pb.matmul(x, w_full, L, 16)
+            _, y_o, _ = orc.pbatch(m, L, 0, 0.25, L, xh, 16, nthreads=8)
+            assert np.array_equal(ref.cpu().numpy().view(np.uint32), y_o.view(np.uint32))
             torch.cuda.synchronize()
             for r in range(N):
                 pb.matmul_rowshard_p2p(x, ws_[r], R, p2ps[r], L, 16, ws=wss[r], stream=streams[r])
@@ -64,6 +69,40 @@ def test_p2p_ranks_on_one_gpu(pb, N, R, K, L, B):
         torch.cuda.synchronize()
         for r in range(N):
             assert torch.equal(p2ps[r].y.view(torch.int32), ref.view(torch.int32)), ("graph", r)
+    finally:
+        torch.cuda.synchronize()
+        for p in p2ps:
+            p.close()
+
+
+@pytest.mark.parametrize("N,R,K,L,B", [(2, 2048, 2048, 4, 1), (4, 1024, 1024, 3, 2)])
+def test_p2p_back_to_back_changing_x(pb, orc, N, R, K, L, B):
+    """Calls n = 0..5 with a different x each, queued without any host sync; after each
+    call every rank's stream copies its y_full out.  A rank that ran ahead must not
+    overwrite a peer's y_full before the peer's copy of call n has run (the entry
+    handshake), so every copy must equal the oracle for its own x."""
+    import torch
+    m = synth.codes(R, K, L, 40 + N)
+    ws_ = [pb.PackedWeights.from_codes(pb.shard_codes(m, N, r), L, 0, 0.25) for r in range(N)]
+    p2ps = pb.P2P.in_process(B, R, N)
+    wss = [pb.Workspace(pb.workspace_bytes(B, K, 16)) for _ in range(N)]
+    streams = [torch.cuda.Stream() for _ in range(N)]
+    calls = 6
+    xs_h = [synth.activations(B, K, 300 + n) for n in range(calls)]
+    xs = [torch.from_numpy(v).cuda() for v in xs_h]
+    outs = [[torch.empty((B, R), device="cuda") for _ in range(calls)] for _ in range(N)]
+    torch.cuda.synchronize()
+    try:
+        for n in range(calls):
+            for r in range(N):
+                pb.matmul_rowshard_p2p(xs[n], ws_[r], R, p2ps[r], L, 16, ws=wss[r], stream=streams[r])
+                with torch.cuda.stream(streams[r]):
+                    outs[r][n].copy_(p2ps[r].y)
+        torch.cuda.synchronize()
+        for n in range(calls):
+            _, y_o, _ = orc.pbatch(m, L, 0, 0.25, L, xs_h[n], 16, nthreads=8)
+            for r in range(N):
+                assert np.array_equal(outs[r][n].cpu().numpy().view(np.uint32), y_o.view(np.uint32)), (n, r)
     finally:
         torch.cuda.synchronize()
         for p in p2ps:
