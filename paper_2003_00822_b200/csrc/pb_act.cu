@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kThreads)
 act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kwords, int a,
                            int act_frac, int words_per_cta, int32_t* __restrict__ f_out,
                            long long* __restrict__ xsum_part, uint32_t* __restrict__ planes,
-                           uint8_t* __restrict__ bexp, int npad, long long* tl)
+                           uint8_t* __restrict__ bexp, int npad, int bs, size_t slice_bytes, long long* tl)
 {
     long long t_launch = 0, t_go = 0;
     if (tl) t_launch = gtimer();
@@ -106,10 +106,15 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
         }
         if (lane < a && w < kwords) pb[(int64_t)lane * kwords + w] = mine;
         if (npad) {
-            // lane j < a writes plane row n = b*a + j; the last batch column zeroes rows [a*B, npad)
-            if (lane < a) put_b_operand(bexp, npad, w, b * a + lane, mine);
-            if (b == (int)gridDim.y - 1)
-                for (int n = (int)gridDim.y * a + lane; n < npad; n += 32) put_b_operand(bexp, npad, w, n, 0u);
+            // lane j < a writes plane row n = b_local*a + j of the column's slice (wide mode:
+            // slices of bs columns, slice-major; narrow: one slice); the slice's last column
+            // zeroes its padding rows [a*nb, npad)
+            const int sl = b / bs, bl = b - sl * bs;
+            const int nb = (int)gridDim.y - sl * bs < bs ? (int)gridDim.y - sl * bs : bs;
+            uint8_t* bx = bexp + (size_t)sl * slice_bytes;
+            if (lane < a) put_b_operand(bx, npad, w, bl * a + lane, mine);
+            if (bl == nb - 1)
+                for (int n = nb * a + lane; n < npad; n += 32) put_b_operand(bx, npad, w, n, 0u);
         }
     }
 #pragma unroll
@@ -176,12 +181,22 @@ cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kword
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // tensor-engine operand tiles: the narrow layout when the whole batch is one launch's
+    // slice, else the wide slice-major layout, else none (POPC engine planes only)
+    int npad = 0, bs = (int)B;
+    size_t slice_bytes = 0;
+    if (l.npad && tc_npad(B, a) == l.npad) {
+        npad = l.npad;
+    } else if (l.wbs) {
+        npad = kTcWideN;
+        bs = l.wbs;
+        slice_bytes = l.wslice_bytes;
+    }
     return cudaLaunchKernelEx(&cfg, act_quant_transpose_kernel, x, K, kwords, a, act_frac, wpc,
                               reinterpret_cast<int32_t*>(base + l.off_f),
                               reinterpret_cast<long long*>(base + l.off_xsum),
                               reinterpret_cast<uint32_t*>(base + l.off_planes),
-                              reinterpret_cast<uint8_t*>(base + l.off_bexp),
-                              tc_npad(B, a) == l.npad ? l.npad : 0, debug_tl());
+                              reinterpret_cast<uint8_t*>(base + l.off_bexp), npad, bs, slice_bytes, debug_tl());
 }
 
 }  // namespace pb

@@ -567,6 +567,7 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     g.xsum = reinterpret_cast<long long*>(base + l.off_xsum);
     g.nsplit = pb::act_nsplit(w->kwords);
     g.B = batch;
+    g.bs = (int)batch;
     g.y = y;
     g.acc = reinterpret_cast<long long*>(acc);
     g.bias = bias;
@@ -574,6 +575,10 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
     g.accumulate = accumulate ? 1 : 0;
     g.mid = (midpoint && k_used < w->layers && !w->offset) ? (1ull << (w->layers - k_used - 1)) : 0ull;
     g.npad = pb::tc_npad(batch, act_bits);     // whole batch in one tensor-engine launch (else 0)
+    if (!g.npad && l.wbs && !x) {              // wide mode: every 128-column slice in one launch
+        g.npad = pb::kTcWideN;
+        g.bs = l.wbs;
+    }
     g.bexp = reinterpret_cast<uint8_t*>(base + l.off_bexp);
     g.accbuf = reinterpret_cast<unsigned long long*>(base + l.off_slots);
     g.counters = reinterpret_cast<int*>(base + l.off_count);
@@ -610,6 +615,7 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
         auto slices_fit = [&](int64_t bs) {
             for (int64_t b0 = 0; b0 < batch; b0 += bs) {
                 gs.B = batch - b0 < bs ? batch - b0 : bs;
+                gs.bs = (int)gs.B;
                 gs.npad = pb::tc_npad(gs.B, act_bits);
                 if (!pb::tc_supported(gs)) return false;
             }
@@ -620,6 +626,7 @@ static pb_status run_gemm(const void* ws, int64_t batch, const pb_weights* w, in
         if (!slices_fit(bs)) return PB_EINVAL;
         for (int64_t b0 = 0; b0 < batch; b0 += bs) {
             gs.B = batch - b0 < bs ? batch - b0 : bs;
+            gs.bs = (int)gs.B;
             gs.npad = pb::tc_npad(gs.B, act_bits);
             gs.x = x + b0 * w->cols;
             gs.y = y + b0 * w->rows;
@@ -696,8 +703,23 @@ static bool tc_fits(const pb_weights* w, int64_t nb, int32_t k_used, int32_t act
     g.k_used = k_used;
     g.a = act_bits;
     g.B = nb;
+    g.bs = (int)nb;
     g.npad = pb::tc_npad(nb, act_bits);
     return g.npad > 0 && pb::tc_supported(g);
+}
+
+// Whether a batch of nb columns runs in wide mode (one launch, 128-column slices).
+static bool tc_fits_wide(const pb_weights* w, int64_t nb, int32_t k_used, int32_t act_bits) {
+    pb::GemmArgs g{};
+    g.R = w->rows;
+    g.kwords = w->kwords;
+    g.L = w->layers;
+    g.k_used = k_used;
+    g.a = act_bits;
+    g.B = nb;
+    g.bs = pb::tc_wide_bs(nb, act_bits);
+    g.npad = pb::kTcWideN;
+    return g.bs > 0 && pb::tc_supported(g);
 }
 
 static pb_status act_and_gemm(const float* x, int64_t batch, const pb_weights* w, int32_t k_used, int32_t act_bits,
@@ -715,6 +737,13 @@ static pb_status act_and_gemm(const float* x, int64_t batch, const pb_weights* w
     if (slice_split < 0) {
         const char* ev = getenv("PB_SLICE_SPLIT");
         slice_split = ev ? atoi(ev) : 1;
+    }
+    if (g_engine != PB_ENGINE_POPC && pb::tc_npad(batch, act_bits) == 0 && tc_fits_wide(w, batch, k_used, act_bits)) {
+        // wide mode: planes + operand tiles of every column in one launch, then one
+        // tensor-engine launch over all 128-column slices
+        if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
+        return run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, nullptr, 0, nullptr, nullptr, nullptr,
+                        midpoint);
     }
     int64_t bs = pb::tc_slice(batch, act_bits);
     while (bs > 1 && !tc_fits(w, bs, k_used, act_bits)) bs = (bs + 1) / 2;   // as the fused path narrows
@@ -872,7 +901,9 @@ pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float*
         const char* ev = getenv("PB_LSTM_SPLIT");   // comparison knob: 0 = always fused, 1 = always split
         split_env = ev ? atoi(ev) : -1;
     }
-    const bool split_first = split_env >= 0 ? split_env > 0 : (batch > 1 && pb::tc_npad(batch, act_bits) > 0);
+    const bool split_first = split_env >= 0 ? split_env > 0
+                                            : (batch > 1 && (pb::tc_npad(batch, act_bits) > 0 ||
+                                                             tc_fits_wide(w_hh, batch, k_used_hh, act_bits)));
     for (int64_t t = 0; t < steps; ++t) {
         const float* h_in = t == 0 ? h0 : h_seq + (t - 1) * batch * H;
         const float* c_in = t == 0 ? c0 : (c_seq ? c_seq + (t - 1) * batch * H : cb[(t - 1) & 1]);

@@ -115,6 +115,10 @@ struct Bars {
     int f[kTcMaxB];                          // f_b
     unsigned long long xs[kTcMaxB];          // this CTA's sum of x_q[b, slice]
     unsigned long long xsum[kTcMaxB];        // sum_c x_q[b, c] over all CTAs
+    // split path (planes by the activation kernel): f_b and sum_c x_q of the current segment's
+    // batch columns, staged once per segment, double-buffered by segment parity
+    int sf[2][kTcMaxB];
+    unsigned long long sxs[2][kTcMaxB];
 };
 static_assert(sizeof(Bars) <= kHdrBytes, "Bars must fit the SMEM header");
 
@@ -286,6 +290,8 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
 // [d_col, d_col + regions*NPAD): one accumulator per group of passes.
 struct TcPlan {
     int tiles;        // ceil(R / 128)
+    int slices;       // batch slices of g.bs columns (wide mode; 1 otherwise): unit u covers global
+                      // tile gt = u / chunks = slice * tiles + row tile, K-chunk u % chunks
     int chunks;       // 32-word K-chunks per tile
     long long units;  // tiles * chunks
     int slots, sf_col, d_col;
@@ -323,6 +329,14 @@ __device__ __forceinline__ void item_units(const TcPlan& p, long long item, long
         u1 = u0 + p.Gu;
         if (u1 > p.units) u1 = p.units;
     }
+}
+// Wide mode: the shared-tile sum slot of global tile gt (static schedule).  Every CTA
+// boundary floor(jU/G) that falls strictly inside the tile's units makes it shared; all
+// contributors name it by the first such boundary j = ceil((gt*chunks + 1) G / U), so the
+// sums need G + 1 slots instead of one per tile.
+__device__ __forceinline__ int shared_slot(const TcPlan& p, long long gt) {
+    const long long t1 = gt * p.chunks + 1;
+    return (int)((t1 * p.gs + p.ustat - 1) / p.ustat);
 }
 // K-chunk of the CTA's first (static) unit.
 __device__ __forceinline__ int first_kc(const TcPlan& p) {
@@ -410,6 +424,64 @@ __device__ __forceinline__ void grid_wait(const int* ctr, unsigned long long bas
     while (ld_acquire_gpu_u64(c) < base + kGridStride) {
     }
 }
+// Epilogue plane sums for a compile-time plane count A (A divides CG): CG accumulator
+// columns hold CG / A batch columns of the slice, plane j of column q at q * A + j.  The
+// plane weights T_0 = -2^(A-1), T_j = 2^(A-1-j) are applied as shifts on
+// independent terms (two interleaved partial sums instead of one serial Horner chain),
+// then the group weight wr; per-column totals go to s_tot [bc][128] (exact modulo 2^64).
+template <int CG, int A>
+__device__ __forceinline__ void plane_sums_ca(uint32_t dreg, int nb, int m, uint32_t s_tot_s,
+                                              unsigned long long wr, bool first) {
+    static_assert(CG % A == 0, "A must divide the column group");
+#pragma unroll 1
+    for (int c0 = 0; c0 < nb * A; c0 += CG) {
+        uint32_t dv[CG];
+        ld_tmem_cols<CG>(dreg + (uint32_t)c0, dv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < CG / A; ++q) {
+            unsigned long long s0 = 0, s1 = 0;
+#pragma unroll
+            for (int j = 0; j < A; ++j) {
+                const unsigned long long v = (unsigned long long)__float2uint_rn(__uint_as_float(dv[q * A + j]));
+                const unsigned long long t = j == 0 ? 0ull - (v << (A - 1)) : (v << (A - 1 - j));
+                if (j & 1) s1 += t;
+                else s0 += t;
+            }
+            const int bc = c0 / A + q;
+            if (bc < nb) {
+                const uint32_t sa = s_tot_s + (uint32_t)(bc * kTcRows + m) * 8u;
+                const unsigned long long t = (s0 + s1) * wr;
+                st_shared_u64(sa, first ? t : t + ld_shared_u64(sa));
+            }
+        }
+    }
+}
+
+// a in {8, 16, 32}: the compile-time form above; false for any other a.
+template <int NPAD>
+__device__ __forceinline__ bool plane_sums_dispatch(int a, uint32_t dreg, int nb, int m, uint32_t s_tot_s,
+                                                    unsigned long long wr, bool first) {
+    constexpr int CG = NPAD < 32 ? NPAD : 32;
+    if (a == 8) {
+        plane_sums_ca<CG, 8>(dreg, nb, m, s_tot_s, wr, first);
+        return true;
+    }
+    if constexpr (CG >= 16) {
+        if (a == 16) {
+            plane_sums_ca<CG, 16>(dreg, nb, m, s_tot_s, wr, first);
+            return true;
+        }
+    }
+    if constexpr (CG >= 32) {
+        if (a == 32) {
+            plane_sums_ca<CG, 32>(dreg, nb, m, s_tot_s, wr, first);
+            return true;
+        }
+    }
+    return false;
+}
+
 // Fused steps a1-a2 (same arithmetic as pb_act.cu), run at
 // kernel start by the 4 epilogue warps (128 threads, bar 5; idle until their first
 // segment) while warp 0 streams weight tiles and the converters already build A
@@ -630,6 +702,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     constexpr uint32_t kBTile = NPAD * 32;                    // one MMA's B (64 columns)
     constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;  // one K-chunk (16 MMAs)
     constexpr int kQConsumers = 2 + kConvWarps + kEpiWarps;   // warps 1, 2, converters, epilogue
+    constexpr bool kWide = NPAD > kTcMaxN;                     // wide mode (split path, static schedule)
     uint8_t* wtile0 = smem + kHdrBytes;
     uint8_t* btile0 = wtile0 + p.wstages * kWTileBytes;
     const uint32_t s_tot_s = smem_u32(btile0 + p.bstages * kBStage);   // [b][128] u64 (B > 1)
@@ -735,7 +808,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             }
             if (u0 < 0) break;
             for (long long u = u0; u < u1; ++u) {
-                const int rt = (int)(u / p.chunks), kc = (int)(u - (long long)rt * p.chunks);
+                const long long gt = u / p.chunks;
+                const int kc = (int)(u - gt * p.chunks), rt = (int)(gt % p.tiles);
                 for (int ps = 0; ps < p.passes; ++ps) {
                     // a stored pair: two 32-word boxes of the pair row; else the canonical last layer
                     const bool stored_pair = 2 * ps + 1 < g.L;
@@ -814,12 +888,14 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             for (int u = it.x; u < it.y; ++u, ++cc) {
                 if (g.x && cc == 0) continue;                 // built in place by the converters
                 wait_published();
-                const int kc = u % p.chunks;
+                const int gt = u / p.chunks, kc = u - gt * p.chunks;
+                const int sl = gt / p.tiles;                  // batch slice (wide mode)
                 const int st = cc % p.bstages;
                 mbar_wait(&bars.b_empty[st], (uint32_t)(((cc / p.bstages) & 1) ^ 1));
                 if (elect_one()) {
                     mbar_arrive_expect_tx(&bars.b_full[st], kBStage);
-                    bulk_g2s(btile0 + st * kBStage, g.bexp + (int64_t)kc * kBStage, kBStage, &bars.b_full[st]);
+                    bulk_g2s(btile0 + st * kBStage, g.bexp + ((int64_t)sl * p.chunks + kc) * kBStage, kBStage,
+                             &bars.b_full[st]);
                 }
                 __syncwarp();
             }
@@ -840,11 +916,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             if (it.x < 0) break;
             for (int u = it.x; u < it.y; ++seg) {
                 // a segment: the item's units in one row tile, accumulated in D[seg & 1]
-                const int rt = u / p.chunks;
-                int ue = (rt + 1) * p.chunks;
+                const int gt = u / p.chunks;
+                int ue = (gt + 1) * p.chunks;
                 if (ue > it.y) ue = it.y;
-                const int db = seg & 1;
-                if (seg >= 2) TWAIT(&bars.d_empty[db], (uint32_t)(((seg >> 1) - 1) & 1), 0);
+                // narrow: D double-buffered by segment parity; wide: one D, drained per segment
+                const int db = kWide ? 0 : (seg & 1);
+                if (kWide ? seg >= 1 : seg >= 2)
+                    TWAIT(&bars.d_empty[db], (uint32_t)((kWide ? seg - 1 : (seg >> 1) - 1) & 1), 0);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(p.d_col + db * p.regions * NPAD);
                 for (const int us = u; u < ue; ++u, ++cc) {
@@ -982,6 +1060,28 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer; + the midpoint offset
         const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0) + g.mid;
         bool have_xsum = false;
+        const int pt = threadIdx.x - kEpi0 * 32;      // 0..127
+        int seg_b0 = 0, spar = 0;                     // current segment: first batch column, parity
+        // split path: stage f_b and sum_c x_q (the activation kernel's per-CTA partials) of the
+        // segment's nb columns in SMEM -- one round of loads per segment, not per row
+        auto stage_cols = [&](int b0, int nb, int par) {
+            if (!g.x && pt < nb) {
+                const long long* xs = g.xsum + (int64_t)(b0 + pt) * kXsumStride;
+                unsigned long long sx = 0;
+                int pp = 0;
+#pragma unroll 1
+                for (; pp + 8 <= g.nsplit; pp += 8) {
+                    long long v[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) v[k] = __ldcg(xs + pp + k);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) sx += (unsigned long long)v[k];
+                }
+                for (; pp < g.nsplit; ++pp) sx += (unsigned long long)__ldcg(xs + pp);
+                bars.sf[par][pt] = __ldcg(g.f + b0 + pt);
+                bars.sxs[par][pt] = sx;
+            }
+        };
         auto xsum_of = [&](int b) -> unsigned long long {
             if (g.x) {
                 if (!have_xsum) {
@@ -990,11 +1090,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 }
                 return bars.xsum[b];
             }
-            unsigned long long sx = 0;
-            const long long* xs = g.xsum + b * kXsumStride;
-#pragma unroll 1
-            for (int pp = 0; pp < g.nsplit; ++pp) sx += (unsigned long long)xs[pp];
-            return sx;
+            return bars.sxs[spar][b - seg_b0];
         };
         // a5: y = dequant(acc) (+ bias, + y when accumulating), then fn -- or, in cell mode
         // (pb_lstm_seq), the LSTM cell over the 4 gate rows of a hidden unit (lanes 4j..4j+3)
@@ -1003,7 +1099,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             const long long accv = (long long)t;
             const int64_t o = (int64_t)b * g.R + row;
             if (g.acc) g.acc[o] = accv;
-            float yv = dequant(accv, g.scale, g.x ? bars.f[b] : g.f[b]);
+            float yv = dequant(accv, g.scale, g.x ? bars.f[b] : bars.sf[spar][b - seg_b0]);
             if (g.bias) yv += g.bias[row];
             if (g.accumulate) yv += g.y[o];
             return yv;
@@ -1068,12 +1164,15 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             const int2 it = take_item(bars, qi, qph, lane);
             if (it.x < 0) break;
             for (int u = it.x; u < it.y; ++seg) {
-                const int rt = u / p.chunks, kcA = u - rt * p.chunks;
-                int ue = (rt + 1) * p.chunks;
+                const int gt = u / p.chunks, kcA = u - gt * p.chunks;
+                const int sl = gt / p.tiles, rt = gt - sl * p.tiles;      // batch slice, row tile
+                const int b0 = sl * g.bs;                                 // the slice's first column
+                const int nb = (int)(g.B - b0 < g.bs ? g.B - b0 : g.bs);  // and its width
+                int ue = (gt + 1) * p.chunks;
                 if (ue > it.y) ue = it.y;
                 const int kcB = kcA + (ue - u);
-                const int db = seg & 1;
-                mbar_wait(&bars.d_full[db], (uint32_t)((seg >> 1) & 1));
+                const int db = kWide ? 0 : (seg & 1);
+                mbar_wait(&bars.d_full[db], (uint32_t)((kWide ? seg : (seg >> 1)) & 1));
                 tc_fence_after();
                 long long te[4] = {0, 0, 0, 0}, tcy[3] = {0, 0, 0};
                 if TLP(g) {
@@ -1089,15 +1188,16 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     int last = (r + 1) * p.Gp - 1;
                     if (last > p.passes - 1) last = p.passes - 1;
                     const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
-                    // all of the region's columns in one batch of loads, one wait
-                    uint32_t dv[NPAD];
-                    ld_tmem_cols<NPAD>(tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD), dv);
-                    tmem_ld_wait();
-                    if (TLP(g) && r == 0) {
-                        te[3] = gtimer();
-                        tcy[1] = clock64();
-                    }
-                    if (g.B == 1) {
+                    const uint32_t dreg = tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD);
+                    if (!kWide && g.B == 1) {
+                        // all of the region's columns in one batch of loads, one wait
+                        uint32_t dv[NPAD];
+                        ld_tmem_cols<NPAD>(dreg, dv);
+                        tmem_ld_wait();
+                        if (TLP(g) && r == 0) {
+                            te[3] = gtimer();
+                            tcy[1] = clock64();
+                        }
                         unsigned long long h = 0ull - (unsigned long long)__float2uint_rn(__uint_as_float(dv[0]));
 #pragma unroll
                         for (int e = 1; e < NPAD; ++e) {
@@ -1105,21 +1205,35 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                             h = (e < g.a) ? h + h + v : h;
                         }
                         tot1 += h * wr;
+                    } else if (plane_sums_dispatch<NPAD>(g.a, dreg, nb, m, s_tot_s, wr, r == 0)) {
                     } else {
+                        // any other a: per batch column, serial Horner; wide: 32 columns per batch
+                        // of loads
+                        constexpr int kCG = kWide ? 32 : NPAD;
                         unsigned long long h = 0;
                         int j = 0, bc = 0;
+#pragma unroll 1
+                        for (int c0 = 0; c0 < NPAD && bc < nb; c0 += kCG) {
+                            uint32_t dv[kCG];
+                            ld_tmem_cols<kCG>(dreg + (uint32_t)c0, dv);
+                            tmem_ld_wait();
+                            if (TLP(g) && r == 0 && c0 == 0) {
+                                te[3] = gtimer();
+                                tcy[1] = clock64();
+                            }
 #pragma unroll
-                        for (int e = 0; e < NPAD; ++e) {
-                            if (bc < g.B) {
-                                const unsigned long long v =
-                                    (unsigned long long)__float2uint_rn(__uint_as_float(dv[e]));
-                                h = j == 0 ? 0ull - v : h + h + v;
-                                if (++j == g.a) {
-                                    const uint32_t sa = s_tot_s + (uint32_t)(bc * kTcRows + m) * 8u;
-                                    const unsigned long long t = h * wr;
-                                    st_shared_u64(sa, r == 0 ? t : t + ld_shared_u64(sa));
-                                    j = 0;
-                                    ++bc;
+                            for (int e = 0; e < kCG; ++e) {
+                                if (bc < nb) {
+                                    const unsigned long long v =
+                                        (unsigned long long)__float2uint_rn(__uint_as_float(dv[e]));
+                                    h = j == 0 ? 0ull - v : h + h + v;
+                                    if (++j == g.a) {
+                                        const uint32_t sa = s_tot_s + (uint32_t)(bc * kTcRows + m) * 8u;
+                                        const unsigned long long t = h * wr;
+                                        st_shared_u64(sa, r == 0 ? t : t + ld_shared_u64(sa));
+                                        j = 0;
+                                        ++bc;
+                                    }
                                 }
                             }
                         }
@@ -1128,24 +1242,31 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.d_empty[db]);
+                stage_cols(b0, nb, seg & 1);
+                seg_b0 = b0;
+                spar = seg & 1;
+                if (!g.x) asm volatile("bar.sync 1, 128;" ::: "memory");
                 if TLP(g) {
                     te[1] = gtimer();
                     tcy[2] = clock64();
                 }
                 // exact integer adds into the tile's accumulator (order-independent); no
                 // round trip here: tiles are finalised after the end-of-work grid barrier
-                unsigned long long* ab = g.accbuf + (int64_t)rt * g.B * kTcRows + m;
+                // shared-tile sums: narrow mode one slot per tile, wide mode one per CTA boundary
+                const long long slot = kWide ? shared_slot(p, gt) : gt;
+                unsigned long long* ab = g.accbuf + slot * g.bs * kTcRows + m;
                 if (p.stat && kcA == 0 && kcB == p.chunks) {
                     // static schedule, the segment is the whole tile: y straight from the sums
                     const int64_t row = (int64_t)rt * kTcRows + m;
-                    for (int b = 0; b < g.B; ++b)
-                        finish_tile_row(b, row,
-                                        g.B == 1 ? tot1 : ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
+                    for (int b = 0; b < nb; ++b)
+                        finish_tile_row(b0 + b, row,
+                                        (!kWide && g.B == 1) ? tot1
+                                                             : ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
                 } else {
-                    if (g.B == 1) {
+                    if (!kWide && g.B == 1) {
                         red_add_u64(ab, tot1);
                     } else {
-                        for (int b = 0; b < g.B; ++b)
+                        for (int b = 0; b < nb; ++b)
                             red_add_u64(ab + b * kTcRows, ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
                     }
                     if (p.stat) {
@@ -1157,19 +1278,19 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                             int old;
                             asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;"
                                          : "=r"(old)
-                                         : "l"(g.counters + rt), "r"(kcB - kcA)
+                                         : "l"(g.counters + slot), "r"(kcB - kcA)
                                          : "memory");
                             bars.fin_tile = (old + (kcB - kcA) == p.chunks) ? rt : -1;
                         }
                         asm volatile("bar.sync 1, 128;" ::: "memory");
                         if (bars.fin_tile >= 0) {
                             const int64_t row = (int64_t)rt * kTcRows + m;
-                            for (int b = 0; b < g.B; ++b) {
+                            for (int b = 0; b < nb; ++b) {
                                 const unsigned long long t = __ldcg(ab + b * kTcRows);
                                 ab[b * kTcRows] = 0;       // every call leaves the accumulators zero
-                                finish_tile_row(b, row, t);
+                                finish_tile_row(b0 + b, row, t);
                             }
-                            if (ew == 0 && lane == 0) g.counters[rt] = 0;
+                            if (ew == 0 && lane == 0) g.counters[slot] = 0;
                         }
                     }
                 }
@@ -1200,6 +1321,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 sys_wait(g.local_ctr + 1, rbase + kGridStride);   // (the static schedule waited above)
             if TLP(g) bars.t_ebar[1] = gtimer();
         }
+        stage_cols(0, (int)g.B, seg & 1);         // (narrow: one slice of all B columns)
+        seg_b0 = 0;
+        spar = seg & 1;
         asm volatile("bar.sync 1, 128;" ::: "memory");
         for (long long rt = blockIdx.x; rt < p.tiles; rt += G) {
             const int64_t row = rt * kTcRows + m;
@@ -1313,11 +1437,17 @@ int ceil_log2_i(int64_t v) {
 // The plan for a shape, or false when the tensor engine does not cover it.
 bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
 {
-    if (npad <= 0 || g.kwords <= 0 || g.R <= 0 || g.B <= 0 || g.B > kTcMaxB || g.L > 16) return false;
+    const bool wide = npad > kTcMaxN;
+    if (npad <= 0 || g.kwords <= 0 || g.R <= 0 || g.B <= 0 || g.L > 16) return false;
+    if (wide ? (npad != kTcWideN || g.x || g.nranks || g.bs < 1 || (int64_t)g.bs * g.a > npad)
+             : (g.B > kTcMaxB))
+        return false;
     p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
-    if (p.tiles > kAccTiles) return false;
+    if (!wide && p.tiles > kAccTiles) return false;
     p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
-    p.units = (long long)p.tiles * p.chunks;
+    p.slices = wide ? (int)((g.B + g.bs - 1) / g.bs) : 1;
+    p.units = (long long)p.slices * p.tiles * p.chunks;
+    if (p.units >= (1ll << 30)) return false;                  // int unit indices in the kernel
     // exact f32 accumulation: a group of G layers sums to < K * 2^G <= 2^24
     int G = 24 - ceil_log2_i(g.kwords * 32);
     if (G > 15) G = 15;                           // SFB exponents 0..13 fit the 64-column SF area
@@ -1326,7 +1456,8 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     p.passes = (g.k_used + 1) / 2;
     p.regions = (p.passes + p.Gp - 1) / p.Gp;
     if (p.regions > kMaxRegions) return false;
-    p.d_col = 512 - (2 * p.regions * npad + 31) / 32 * 32;   // two accumulator sets
+    // narrow: two accumulator sets (segment parity); wide: one
+    p.d_col = 512 - ((wide ? 1 : 2) * p.regions * npad + 31) / 32 * 32;
     p.sf_col = p.d_col - 64;
     p.slots = p.sf_col / 128;
     if (p.slots > kMaxSlots) p.slots = kMaxSlots;
@@ -1344,7 +1475,7 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
 // each).  Devices are few; the table is written once per (device, NPAD) under a mutex.
 struct DevState {
     int sms = 0;
-    bool attr[4] = {false, false, false, false};
+    bool attr[5] = {false, false, false, false, false};
 };
 constexpr int kMaxDevices = 64;
 DevState g_dev[kMaxDevices];
@@ -1411,7 +1542,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     if (e != cudaSuccess) return e;
     if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
     DevState& ds = g_dev[dev];
-    constexpr int ai = NPAD == 8 ? 0 : (NPAD == 16 ? 1 : (NPAD == 32 ? 2 : 3));
+    constexpr int ai = NPAD == 8 ? 0 : (NPAD == 16 ? 1 : (NPAD == 32 ? 2 : (NPAD == 64 ? 3 : 4)));
     if (!ds.attr[ai] || !ds.sms) {
         std::lock_guard<std::mutex> lk(g_dev_mu);
         if (!ds.sms) {
@@ -1431,7 +1562,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     const int sms = ds.sms;
     TcPlan p;
     if (!make_plan(g, NPAD, p)) return cudaErrorNotSupported;
-    if (stat_env != 0) {                       // default: static (PB_TC_STATIC=0: dynamic claims)
+    if (stat_env != 0 || NPAD > kTcMaxN) {     // default: static (PB_TC_STATIC=0: dynamic claims)
         p.stat = 1;
         p.gs = (int)(p.units < sms ? p.units : sms);
         if (p.gs > kMaxCtas) p.gs = kMaxCtas;
@@ -1448,9 +1579,10 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     p.dbg = dbg;
     p.prof = prof;
     // weight ring: every 16 KiB stage the B stages and epilogue sums leave free
-    p.bstages = p.passes <= 2 ? kMaxBStages : 2;
+    p.bstages = (p.passes <= 2 && NPAD <= kTcMaxN) ? kMaxBStages : 2;
     if (bst_env) p.bstages = bst_env < 2 ? 2 : (bst_env > kMaxBStages ? kMaxBStages : bst_env);
-    const uint32_t fixed = 1024 + kHdrBytes + (uint32_t)p.bstages * (kChunkWords / 2) * NPAD * 32 + (uint32_t)g.B * kTcRows * 8;
+    if (NPAD > kTcMaxN && p.bstages > 2) p.bstages = 2;        // 64 KiB per wide B stage
+    const uint32_t fixed = 1024 + kHdrBytes + (uint32_t)p.bstages * (kChunkWords / 2) * NPAD * 32 + (uint32_t)g.bs * kTcRows * 8;
     p.wstages = (int)((kSmemMax - fixed) / kWTileBytes);
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     if (p.wstages < 4) return cudaErrorNotSupported;
@@ -1486,6 +1618,7 @@ cudaError_t launch_gemm_tc(const GemmArgs& g, cudaStream_t s)
         case 16: return launch_t<16>(g, s);
         case 32: return launch_t<32>(g, s);
         case 64: return launch_t<64>(g, s);
+        case kTcWideN: return launch_t<kTcWideN>(g, s);
         default: return cudaErrorNotSupported;
     }
 }

@@ -13,6 +13,8 @@ constexpr size_t kAlign = 256;
 constexpr int kTcRows = 128;         // tensor engine row tile (MMA M)
 constexpr int kTcMaxN = 64;          // tensor engine: a * batch <= 64 per launch (MMA N padded to 8/16/32/64)
 constexpr int kTcMaxB = 32;          // tensor engine: batch columns per launch
+constexpr int kTcWideN = 128;        // wide mode: MMA N = 128 plane columns per slice, every slice
+                                     // of the batch in one launch (single-buffered accumulator)
 constexpr int kMaxRanks = 8;         // pb_matmul_rowshard_p2p: ranks of one node
 
 inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
@@ -31,6 +33,13 @@ inline int64_t tc_slice(int64_t batch, int32_t a) {
     int64_t s = kTcMaxN / a;
     if (s > kTcMaxB) s = kTcMaxB;
     return s < 1 ? 1 : s;
+}
+
+// Wide mode (a*batch > 64, 8 <= a <= 32): batch columns per 128-column slice, else 0.
+// (a >= 8 keeps the per-slice epilogue sums, <= 16 x 1 KiB of SMEM, beside >= 4 weight stages.)
+inline int tc_wide_bs(int64_t batch, int32_t a) {
+    if (a < 8 || a > 32 || tc_npad(batch, a) > 0 || batch <= 0) return 0;
+    return kTcWideN / a;
 }
 
 // Workspace carve-up (documented in pb.h, pb_workspace_bytes):
@@ -55,7 +64,10 @@ constexpr int kXsumStride = kMaxCtas;   // Σx_q partials per batch column (act 
 constexpr int kAccTiles = 2048;      // tensor engine: rows <= 2048 * 128 (partial-tile accumulators)
 struct WsLayout {
     size_t off_count, off_slots, off_f, off_xsum, off_planes, off_bexp, total;
-    int npad;
+    int npad;                 // narrow: MMA N of one launch's slice (0: no narrow operand tiles)
+    int wbs;                  // wide mode: batch columns per slice (0: off); operand tiles are
+    int64_t wslices;          //   slice-major, [slice][chunk][16 words-pairs][128 x 32 B]
+    size_t wslice_bytes;
 };
 inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     WsLayout l;
@@ -70,12 +82,19 @@ inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     if (bs_max > kTcMaxB) bs_max = kTcMaxB;
     if (bs_max < 1) bs_max = 1;
     if (bs_max < bs) bs_max = bs;
-    const size_t slots = l.npad ? sizeof(long long) * kAccTiles * (size_t)bs_max * kTcRows : 0;
+    l.wbs = tc_wide_bs(batch, act_bits);
+    l.wslices = l.wbs ? (batch + l.wbs - 1) / l.wbs : 0;
+    l.wslice_bytes = (size_t)((kwords + 31) / 32 * 32) * 16 * kTcWideN;
+    // wide mode indexes its shared-tile sums by the CTA boundary inside the tile
+    // (<= kMaxCtas + 1 slots of wbs x 128), which always fits the narrow region
+    const size_t slots = (l.npad || l.wbs) ? sizeof(long long) * kAccTiles * (size_t)bs_max * kTcRows : 0;
     l.off_f = align_up(l.off_slots + slots);
     l.off_xsum = align_up(l.off_f + sizeof(int32_t) * (size_t)batch);
     l.off_planes = align_up(l.off_xsum + sizeof(long long) * (size_t)batch * kXsumStride);
     l.off_bexp = align_up(l.off_planes + sizeof(uint32_t) * (size_t)batch * act_bits * kwords);
-    l.total = align_up(l.off_bexp + (size_t)((kwords + 31) / 32 * 32) * 16 * (size_t)l.npad);
+    size_t bexp = (size_t)((kwords + 31) / 32 * 32) * 16 * (size_t)l.npad;
+    if (l.wbs && (size_t)l.wslices * l.wslice_bytes > bexp) bexp = (size_t)l.wslices * l.wslice_bytes;
+    l.total = align_up(l.off_bexp + bexp);
     return l;
 }
 
@@ -96,6 +115,7 @@ struct GemmArgs {
     long long* xsum;        // [B][kXsumStride], nsplit used
     int nsplit;
     int64_t B;
+    int bs;                 // batch columns per slice: B (narrow, one slice) or kTcWideN / a (wide)
     float* y;               // [B][R]
     long long* acc;         // [B][R] or null
     const float* bias;      // [R] or null

@@ -73,6 +73,13 @@ CASES = [  # R, K, B, L, k_used, a
     (129, 3000, 8, 8, 7, 8),      # N = 64, a = 8
     (200, 1500, 37, 4, 4, 16),    # 10 slices of <= 4 columns, ragged last slice
     (512, 2048, 8, 16, 16, 16),   # 2 accumulator groups: N = 64 slices narrowed to N = 32
+    # wide mode (a*B > 64, a >= 8): every 128-plane-column slice in one launch
+    (300, 2000, 9, 8, 8, 16),     # 2 slices (8 + 1 columns), ragged K
+    (1000, 4109, 40, 6, 5, 8),    # a = 8: 3 slices of 16/16/8, odd k_used
+    (129, 3000, 24, 4, 4, 32),    # a = 32: 6 slices of 4
+    (2048, 1024, 128, 2, 2, 16),  # 16 slices, 512 units over the grid
+    (700, 5000, 19, 12, 11, 10),  # a = 10: slices of 12 columns (120 rows + 8 padding), 2 slices
+    (257, 1030, 17, 1, 1, 16),    # L = 1 (canonical single layer) in wide mode
 ]
 
 
