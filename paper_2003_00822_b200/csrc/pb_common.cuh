@@ -138,6 +138,14 @@ __device__ __forceinline__ float dequant(long long acc, double scale, int f) {
     t = ldexp(t, -f);
     return __double2float_rn(t);
 }
+// The same with the column's scale folded: y = (float)((double)acc * (s_w 2^-f_b)).  Scaling
+// by an exact power of two commutes with round-to-nearest while nothing under- or overflows
+// (here |acc| < 2^63, s_w >= 2^-170 and f_b in [-130, 180] keep every value normal), so this
+// is bit-identical to dequant() with one FP64 multiply fewer (col_scale is exact).
+__device__ __forceinline__ double col_scale(double scale, int f) { return ldexp(scale, -f); }
+__device__ __forceinline__ float dequant_sc(long long acc, double sc) {
+    return __double2float_rn(__dmul_rn(__ll2double_rn(acc), sc));
+}
 // LSTM cell (reading G15: PyTorch nn.LSTM gates i, f, g, o; fp32 as P:128 keeps the
 // nonlinearities in full precision): c' = sigmoid(f) c + sigmoid(i) tanh(g),
 // h' = sigmoid(o) tanh(c').

@@ -111,13 +111,14 @@ struct Bars {
     long long t_c0, t_cv[4];                 // first chunk built; converter warp 3's first pass
     long long t_c0s[2];                      // first chunk: x loads issued, f_b available
     // fused activation prologue
-    float red[12 * kTcMaxB];                 // per-warp partial max|x[b,:]| (prologue warps)
+    float red[kEpiWarps * kTcMaxB];          // per-warp partial max|x[b,:]| (prologue warps)
     int f[kTcMaxB];                          // f_b
+    double fsc[kTcMaxB];                     // s_w 2^-f_b (dequant scale of column b)
     unsigned long long xs[kTcMaxB];          // this CTA's sum of x_q[b, slice]
     unsigned long long xsum[kTcMaxB];        // sum_c x_q[b, c] over all CTAs
     // split path (planes by the activation kernel): f_b and sum_c x_q of the current segment's
     // batch columns, staged once per segment, double-buffered by segment parity
-    int sf[2][kTcMaxB];
+    double ssc[2][kTcMaxB];                  // s_w 2^-f_b
     unsigned long long sxs[2][kTcMaxB];
 };
 static_assert(sizeof(Bars) <= kHdrBytes, "Bars must fit the SMEM header");
@@ -567,6 +568,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
 #pragma unroll
         for (int w = 1; w < kPW; ++w) m = fmaxf(m, bars.red[w * kTcMaxB + pt]);
         bars.f[pt] = (g.act_frac == kActAutoFrac) ? act_frac_of(m, g.a) : g.act_frac;
+        bars.fsc[pt] = col_scale(g.scale, bars.f[pt]);
         bars.xs[pt] = 0;
     }
     asm volatile("bar.sync 5, 128;" ::: "memory");
@@ -1078,7 +1080,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     for (int k = 0; k < 8; ++k) sx += (unsigned long long)v[k];
                 }
                 for (; pp < g.nsplit; ++pp) sx += (unsigned long long)__ldcg(xs + pp);
-                bars.sf[par][pt] = __ldcg(g.f + b0 + pt);
+                bars.ssc[par][pt] = col_scale(g.scale, __ldcg(g.f + b0 + pt));
                 bars.sxs[par][pt] = sx;
             }
         };
@@ -1099,15 +1101,17 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             const long long accv = (long long)t;
             const int64_t o = (int64_t)b * g.R + row;
             if (g.acc) g.acc[o] = accv;
-            float yv = dequant(accv, g.scale, g.x ? bars.f[b] : bars.sf[spar][b - seg_b0]);
+            float yv = dequant_sc(accv, g.x ? bars.fsc[b] : bars.ssc[spar][b - seg_b0]);
             if (g.bias) yv += g.bias[row];
             if (g.accumulate) yv += g.y[o];
             return yv;
         };
-        auto finish_tile_row = [&](int b, int64_t row, unsigned long long t) {   // warp-uniform call
+        // the rest of a5 for one column given its pre-activation: fn and the y store (or the
+        // peer stores), or in cell mode the LSTM cell (warp-uniform call: lane shuffles)
+        auto finish_value = [&](int b, int64_t row, float pre) {
             if (!g.cell) {
                 if (row < g.R) {
-                    const float v = apply_fn(preact(b, row, t), g.fn);
+                    const float v = apply_fn(pre, g.fn);
                     if (g.nranks) {
                         // fused all-gather (f2): this row of y into every rank's y_full
                         const int64_t grow = g.row0 + row;
@@ -1119,7 +1123,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 }
                 return;
             }
-            const float v = row < g.R ? preact(b, row, t) : 0.f;
+            const float v = pre;
             const int q0 = lane & ~3;
             const float gi = __shfl_sync(0xffffffffu, v, q0), gf = __shfl_sync(0xffffffffu, v, q0 + 1);
             const float gg = __shfl_sync(0xffffffffu, v, q0 + 2), go = __shfl_sync(0xffffffffu, v, q0 + 3);
@@ -1129,6 +1133,23 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 lstm_cell(gi, gf, gg, go, g.cell_c[i], hn, cn);
                 g.cell_h[i] = hn;
                 g.cell_c_out[i] = cn;
+            }
+        };
+        auto finish_tile_row = [&](int b, int64_t row, unsigned long long t) {   // warp-uniform call
+            finish_value(b, row, row < g.R ? preact(b, row, t) : 0.f);
+        };
+        // columns [b0, b0 + nb) of this thread's row, totals from get_t(local column): the
+        // pre-activations of 8 columns at a time are independent chains (the FP64 conversion
+        // and multiply have long latencies), then finished one column at a time
+        auto finish_cols = [&](int b0, int nb, int64_t row, auto&& get_t) {   // warp-uniform call
+#pragma unroll 1
+            for (int bg = 0; bg < nb; bg += 8) {
+                float v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    v[k] = (bg + k < nb && row < g.R) ? preact(b0 + bg + k, row, get_t(bg + k)) : 0.f;
+#pragma unroll 1
+                for (int k = 0; k < 8 && bg + k < nb; ++k) finish_value(b0 + bg + k, row, v[k]);
             }
         };
         if (g.x)
@@ -1258,10 +1279,11 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 if (p.stat && kcA == 0 && kcB == p.chunks) {
                     // static schedule, the segment is the whole tile: y straight from the sums
                     const int64_t row = (int64_t)rt * kTcRows + m;
-                    for (int b = 0; b < nb; ++b)
-                        finish_tile_row(b0 + b, row,
-                                        (!kWide && g.B == 1) ? tot1
-                                                             : ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u));
+                    if (!kWide && g.B == 1)
+                        finish_tile_row(0, row, tot1);
+                    else
+                        finish_cols(b0, nb, row,
+                                    [&](int b) { return ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u); });
                 } else {
                     if (!kWide && g.B == 1) {
                         red_add_u64(ab, tot1);
@@ -1285,11 +1307,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         asm volatile("bar.sync 1, 128;" ::: "memory");
                         if (bars.fin_tile >= 0) {
                             const int64_t row = (int64_t)rt * kTcRows + m;
-                            for (int b = 0; b < nb; ++b) {
-                                const unsigned long long t = __ldcg(ab + b * kTcRows);
-                                ab[b * kTcRows] = 0;       // every call leaves the accumulators zero
-                                finish_tile_row(b0 + b, row, t);
-                            }
+                            finish_cols(b0, nb, row, [&](int b) { return __ldcg(ab + b * kTcRows); });
+                            for (int b = 0; b < nb; ++b) ab[b * kTcRows] = 0;   // leave the sums zero
                             if (ew == 0 && lane == 0) g.counters[slot] = 0;
                         }
                     }
@@ -1328,11 +1347,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         for (long long rt = blockIdx.x; rt < p.tiles; rt += G) {
             const int64_t row = rt * kTcRows + m;
             unsigned long long* ab = g.accbuf + rt * g.B * kTcRows + m;
-            for (int b = 0; b < g.B; ++b) {
-                const unsigned long long t = __ldcg(ab + b * kTcRows);
-                ab[b * kTcRows] = 0;                  // every call leaves the accumulators zero
-                finish_tile_row(b, row, t);
-            }
+            finish_cols(0, (int)g.B, row, [&](int b) { return __ldcg(ab + b * kTcRows); });
+            for (int b = 0; b < g.B; ++b) ab[b * kTcRows] = 0;   // every call leaves the sums zero
         }
         }   // !p.stat
         if (g.nranks) {
