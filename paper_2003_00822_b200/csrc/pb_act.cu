@@ -106,15 +106,17 @@ act_quant_transpose_kernel(const float* __restrict__ x, int64_t K, int64_t kword
         }
         if (lane < a && w < kwords) pb[(int64_t)lane * kwords + w] = mine;
         if (npad) {
-            // lane j < a writes plane row n = b_local*a + j of the column's slice (wide mode:
+            // lane 2k < a writes digit row n = b_local*nd + k of the column's slice (wide mode:
             // slices of bs columns, slice-major; narrow: one slice); the slice's last column
-            // zeroes its padding rows [a*nb, npad)
+            // zeroes its padding rows [nd*nb, npad)
+            const int nd = act_digits(a);
             const int sl = b / bs, bl = b - sl * bs;
             const int nb = (int)gridDim.y - sl * bs < bs ? (int)gridDim.y - sl * bs : bs;
             uint8_t* bx = bexp + (size_t)sl * slice_bytes;
-            if (lane < a) put_b_operand(bx, npad, w, bl * a + lane, mine);
+            uint4 dv;
+            if (digit_of_lane(mine, lane, a, dv)) put_b_operand(bx, npad, w, bl * nd + (lane >> 1), dv);
             if (bl == nb - 1)
-                for (int n = nb * a + lane; n < npad; n += 32) put_b_operand(bx, npad, w, n, 0u);
+                for (int n = nb * nd + lane; n < npad; n += 32) put_b_operand(bx, npad, w, n, make_uint4(0, 0, 0, 0));
         }
     }
 #pragma unroll

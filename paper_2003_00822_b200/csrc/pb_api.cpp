@@ -745,6 +745,13 @@ static pb_status act_and_gemm(const float* x, int64_t batch, const pb_weights* w
         return run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, nullptr, 0, nullptr, nullptr, nullptr,
                         midpoint);
     }
+    if (slice_split && batch > 1 && g_engine != PB_ENGINE_POPC && tc_fits(w, batch, k_used, act_bits)) {
+        // a batch that fits one narrow launch: planes kernel + one GEMM launch (the fused
+        // prologue's per-column work on every CTA is the longer path once batch > 1)
+        if ((st = pb_act_quantize(x, batch, w->cols, act_bits, act_frac, ws, ws_bytes, s)) != PB_OK) return st;
+        return run_gemm(ws, batch, w, k_used, act_bits, y, acc, bias, fn, 0, s, nullptr, 0, nullptr, nullptr, nullptr,
+                        midpoint);
+    }
     int64_t bs = pb::tc_slice(batch, act_bits);
     while (bs > 1 && !tc_fits(w, bs, k_used, act_bits)) bs = (bs + 1) / 2;   // as the fused path narrows
     if (slice_split && bs < batch && g_engine != PB_ENGINE_POPC && tc_fits(w, bs, k_used, act_bits) &&

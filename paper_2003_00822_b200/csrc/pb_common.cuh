@@ -90,25 +90,50 @@ __device__ __forceinline__ int act_frac_of(float m, int a) {
     frexpf(m, &e);           // m = frac * 2^e, frac in [0.5, 1): m < 2^e
     return (a - 1) - e;
 }
-// Tensor-engine B operand (pb_gemm_tc.cu): plane word p of plane row n for
-// word w, as 4 uint32 of e2m1 nibbles (X bit (4e + r) -> 2.0 = 0b0100) in the
-// K-major no-swizzle canonical layout of the N_pad x 32-byte tile of words
-// (w & ~1, w | 1).
-__device__ __forceinline__ void put_b_operand(uint8_t* bexp, int npad, int64_t w, int n, uint32_t p) {
-    uint8_t* tile = bexp + (w >> 1) * npad * 32 + (w & 1) * 128;
-    *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + (n & 7) * 16) =
-        make_uint4((p & 0x11111111u) << 2, ((p >> 1) & 0x11111111u) << 2, ((p >> 2) & 0x11111111u) << 2,
-                   ((p >> 3) & 0x11111111u) << 2);
+// Tensor-engine B operand (pb_gemm_tc.cu): the activation planes stacked in pairs (the
+// "multiple bitlayers may be stacked together" of P:206, applied to the activation side as
+// it is to the weights): digit k of a column is d_k = 2 X_2k + X_2k+1 with weight
+// U_k = 2^(a-2-2k), the sign pair carries its negative plane weight, d_0 = -2 X_0 + X_1,
+// and an odd a leaves the last plane alone, d = X_(a-1) with U = 1 (a = 1: d_0 = -X_0).
+// Then sum_k U_k d_k = sum_j T_j X_j = x_q exactly (T_0 = -2^(a-1), T_j = 2^(a-1-j)).
+// Each digit is stored as the e2m1 value 2 d in {-4, -2, 0, 2, 4, 6} (exact), so against a
+// weight nibble 1.0 hi + 0.5 lo the product is the integer (2 hi + lo) d.
+__host__ __device__ constexpr int act_digits(int a) { return (a + 1) / 2; }
+// 4 registers of e2m1 nibbles (register r, nibble e <-> column 4e + r of the 32-column word)
+// from the digit's plane words hi (X_2k) and lo (X_2k+1); branch-free over the kinds with
+// ms = sign digit, ml = lone plane (all-ones masks): bit 3 = sign, bit 2 = any,
+// bit 1 = 2d >= 4 or the sign pair's -4, bit 0 = 2d = 6.
+__device__ __forceinline__ uint4 digit_regs(uint32_t hi, uint32_t lo, uint32_t ms, uint32_t ml) {
+    uint32_t v[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t H = (hi >> r) & 0x11111111u, Lo = (lo >> r) & 0x11111111u & ~ml;
+        const uint32_t b3 = H & ms, b2 = H | Lo, b1 = H & ~ml & (~ms | ~Lo), b0 = H & Lo & ~ms;
+        v[r] = (b3 << 3) | (b2 << 2) | (b1 << 1) | b0;
+    }
+    return make_uint4(v[0], v[1], v[2], v[3]);
 }
-
-// The same B operand word into a shared-memory tile (explicit st.shared: a generic store
-// would resolve its address space at run time).
-__device__ __forceinline__ void put_b_operand_smem(uint32_t tile_s, int npad, int64_t w, int n, uint32_t p) {
+// Digit row n of word w into the K-major no-swizzle canonical layout of the N_pad x 32-byte
+// tile of words (w & ~1, w | 1).
+__device__ __forceinline__ void put_b_operand(uint8_t* bexp, int npad, int64_t w, int n, uint4 v) {
+    uint8_t* tile = bexp + (w >> 1) * npad * 32 + (w & 1) * 128;
+    *reinterpret_cast<uint4*>(tile + (n >> 3) * 256 + (n & 7) * 16) = v;
+}
+// The same into a shared-memory tile (explicit st.shared: a generic store would resolve its
+// address space at run time).
+__device__ __forceinline__ void put_b_operand_smem(uint32_t tile_s, int npad, int64_t w, int n, uint4 v) {
     const uint32_t a = tile_s + (uint32_t)((w >> 1) * npad * 32 + (w & 1) * 128 + (n >> 3) * 256 + (n & 7) * 16);
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"((p & 0x11111111u) << 2),
-                 "r"(((p >> 1) & 0x11111111u) << 2), "r"(((p >> 2) & 0x11111111u) << 2),
-                 "r"(((p >> 3) & 0x11111111u) << 2)
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
+}
+// After a ballot transpose (lane j < a holds plane word j of a 32-column word): the lanes
+// 2k < a hold digit k's registers (the pair partner's plane comes from lane 2k + 1).
+// Warp-collective; returns whether this lane writes digit lane / 2.
+__device__ __forceinline__ bool digit_of_lane(uint32_t mine, int lane, int a, uint4& v) {
+    const uint32_t partner = __shfl_down_sync(0xffffffffu, mine, 1);
+    if ((lane & 1) || lane >= a) return false;
+    v = digit_regs(mine, partner, lane == 0 ? ~0u : 0u, lane == a - 1 ? ~0u : 0u);
+    return true;
 }
 
 // Next diagnostics-timeline record (pb_internal.h, pb_debug_timeline) or null when full.

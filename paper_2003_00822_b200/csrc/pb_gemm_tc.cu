@@ -425,31 +425,34 @@ __device__ __forceinline__ void grid_wait(const int* ctr, unsigned long long bas
     while (ld_acquire_gpu_u64(c) < base + kGridStride) {
     }
 }
-// Epilogue plane sums for a compile-time plane count A (A divides CG): CG accumulator
-// columns hold CG / A batch columns of the slice, plane j of column q at q * A + j.  The
-// plane weights T_0 = -2^(A-1), T_j = 2^(A-1-j) are applied as shifts on
-// independent terms (two interleaved partial sums instead of one serial Horner chain),
+// An accumulator column as a signed integer (|D| < 2^24: exact in f32).
+__device__ __forceinline__ unsigned long long d2i(uint32_t bits) {
+    return (unsigned long long)(long long)__float2int_rn(__uint_as_float(bits));
+}
+// Epilogue digit sums for a compile-time even a = 2 ND (ND divides CG): CG accumulator
+// columns hold CG / ND batch columns of the slice, digit k of column q at q * ND + k.  The
+// digit weights U_k = 4^(ND-1-k) (pb_common.cuh; the sign rides in digit 0) are applied as
+// shifts on independent terms (two interleaved partial sums, not one serial Horner chain),
 // then the group weight wr; per-column totals go to s_tot [bc][128] (exact modulo 2^64).
-template <int CG, int A>
+template <int CG, int ND>
 __device__ __forceinline__ void plane_sums_ca(uint32_t dreg, int nb, int m, uint32_t s_tot_s,
                                               unsigned long long wr, bool first) {
-    static_assert(CG % A == 0, "A must divide the column group");
+    static_assert(CG % ND == 0, "ND must divide the column group");
 #pragma unroll 1
-    for (int c0 = 0; c0 < nb * A; c0 += CG) {
+    for (int c0 = 0; c0 < nb * ND; c0 += CG) {
         uint32_t dv[CG];
         ld_tmem_cols<CG>(dreg + (uint32_t)c0, dv);
         tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < CG / A; ++q) {
+        for (int q = 0; q < CG / ND; ++q) {
             unsigned long long s0 = 0, s1 = 0;
 #pragma unroll
-            for (int j = 0; j < A; ++j) {
-                const unsigned long long v = (unsigned long long)__float2uint_rn(__uint_as_float(dv[q * A + j]));
-                const unsigned long long t = j == 0 ? 0ull - (v << (A - 1)) : (v << (A - 1 - j));
-                if (j & 1) s1 += t;
+            for (int k = 0; k < ND; ++k) {
+                const unsigned long long t = d2i(dv[q * ND + k]) << (2 * (ND - 1 - k));
+                if (k & 1) s1 += t;
                 else s0 += t;
             }
-            const int bc = c0 / A + q;
+            const int bc = c0 / ND + q;
             if (bc < nb) {
                 const uint32_t sa = s_tot_s + (uint32_t)(bc * kTcRows + m) * 8u;
                 const unsigned long long t = (s0 + s1) * wr;
@@ -458,25 +461,22 @@ __device__ __forceinline__ void plane_sums_ca(uint32_t dreg, int nb, int m, uint
         }
     }
 }
-
 // a in {8, 16, 32}: the compile-time form above; false for any other a.
 template <int NPAD>
 __device__ __forceinline__ bool plane_sums_dispatch(int a, uint32_t dreg, int nb, int m, uint32_t s_tot_s,
                                                     unsigned long long wr, bool first) {
     constexpr int CG = NPAD < 32 ? NPAD : 32;
     if (a == 8) {
+        plane_sums_ca<CG, 4>(dreg, nb, m, s_tot_s, wr, first);
+        return true;
+    }
+    if (a == 16) {
         plane_sums_ca<CG, 8>(dreg, nb, m, s_tot_s, wr, first);
         return true;
     }
     if constexpr (CG >= 16) {
-        if (a == 16) {
-            plane_sums_ca<CG, 16>(dreg, nb, m, s_tot_s, wr, first);
-            return true;
-        }
-    }
-    if constexpr (CG >= 32) {
         if (a == 32) {
-            plane_sums_ca<CG, 32>(dreg, nb, m, s_tot_s, wr, first);
+            plane_sums_ca<CG, 16>(dreg, nb, m, s_tot_s, wr, first);
             return true;
         }
     }
@@ -503,6 +503,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     constexpr int kPT = 32 * kPW;
     constexpr int kCx = 8;                             // first-chunk values prefetched per thread
     const int pw = pt >> 5, lane = pt & 31;
+    const int nd = act_digits(g.a);                    // digit rows per batch column
     long long tpw = 0, tmax = 0, tc0 = 0, ttr = 0, tfb = 0, tcg = 0, cyc_ballot = 0, cyc_put = 0;
     pdl_wait();                                        // x may be the previous kernel's output
     if TLP(g) tpw = gtimer();
@@ -597,9 +598,10 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         const long long q = act_cast(v, bars.f[b], g.a);
         uint32_t mine, dummy;
         transpose2(q, 0, mine, dummy);
-        if (lane < g.a) put_b_operand(g.bexp, NPAD, w, b * g.a + lane, mine);
+        uint4 dv;
+        if (digit_of_lane(mine, lane, g.a, dv)) put_b_operand(g.bexp, NPAD, w, b * nd + (lane >> 1), dv);
         if (b == B - 1)
-            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand(g.bexp, NPAD, w, n, 0u);
+            for (int n = B * nd + lane; n < NPAD; n += 32) put_b_operand(g.bexp, NPAD, w, n, make_uint4(0, 0, 0, 0));
         long long xs = q;
 #pragma unroll
         for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
@@ -620,9 +622,11 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     const uint32_t bstage0_s = smem_u32(bstage0);
     auto put0 = [&](int it, uint32_t mine) {
         const int b = it / kChunkWords, wl = it - b * kChunkWords;
-        if (lane < g.a) put_b_operand_smem(bstage0_s, NPAD, wl, b * g.a + lane, mine);
+        uint4 dv;
+        if (digit_of_lane(mine, lane, g.a, dv)) put_b_operand_smem(bstage0_s, NPAD, wl, b * nd + (lane >> 1), dv);
         if (b == B - 1)
-            for (int n = B * g.a + lane; n < NPAD; n += 32) put_b_operand_smem(bstage0_s, NPAD, wl, n, 0u);
+            for (int n = B * nd + lane; n < NPAD; n += 32)
+                put_b_operand_smem(bstage0_s, NPAD, wl, n, make_uint4(0, 0, 0, 0));
     };
     // kCx items (itb + kPW * k) per step: kCx independent ballot chains in flight
     auto chunk_group = [&](int itb, const float (&v)[kCx]) {
@@ -1063,6 +1067,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0) + g.mid;
         bool have_xsum = false;
         const int pt = threadIdx.x - kEpi0 * 32;      // 0..127
+        const int nd = act_digits(g.a);               // activation digits per batch column
         int seg_b0 = 0, spar = 0;                     // current segment: first batch column, parity
         // split path: stage f_b and sum_c x_q (the activation kernel's per-CTA partials) of the
         // segment's nb columns in SMEM -- one round of loads per segment, not per row
@@ -1141,16 +1146,40 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // columns [b0, b0 + nb) of this thread's row, totals from get_t(local column): the
         // pre-activations of 8 columns at a time are independent chains (the FP64 conversion
         // and multiply have long latencies), then finished one column at a time
-        auto finish_cols = [&](int b0, int nb, int64_t row, auto&& get_t) {   // warp-uniform call
+        // (the totals are this thread's s_tot slots [b][m]; each slot is reused for its
+        // pre-activation, so the column loop needs no indexed registers)
+        auto finish_cols = [&](int b0, int nb, int64_t row) {   // warp-uniform call
 #pragma unroll 1
             for (int bg = 0; bg < nb; bg += 8) {
-                float v[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    v[k] = (bg + k < nb && row < g.R) ? preact(b0 + bg + k, row, get_t(bg + k)) : 0.f;
+                for (int k = 0; k < 8; ++k) {
+                    const uint32_t sa = s_tot_s + (uint32_t)((bg + k) * kTcRows + m) * 8u;
+                    if (bg + k < nb && row < g.R)
+                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(sa), "f"(preact(b0 + bg + k, row, ld_shared_u64(sa)))
+                                     : "memory");
+                }
 #pragma unroll 1
-                for (int k = 0; k < 8 && bg + k < nb; ++k) finish_value(b0 + bg + k, row, v[k]);
+                for (int k = 0; k < 8 && bg + k < nb; ++k) {
+                    float v;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(s_tot_s + (uint32_t)((bg + k) * kTcRows + m) * 8u)
+                                 : "memory");
+                    finish_value(b0 + bg + k, row, row < g.R ? v : 0.f);
+                }
             }
+        };
+        // a tile's exact sums from the workspace into s_tot (re-zeroing them), then finished
+        auto finish_from_accbuf = [&](int b0, int nb, int64_t row, unsigned long long* ab) {
+            if (!kWide && g.B == 1) {
+                const unsigned long long t = __ldcg(ab);
+                *ab = 0;                                          // leave the sums zero
+                finish_tile_row(0, row, t);
+                return;
+            }
+            for (int b = 0; b < nb; ++b) {
+                st_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u, __ldcg(ab + b * kTcRows));
+                ab[b * kTcRows] = 0;                              // leave the sums zero
+            }
+            finish_cols(b0, nb, row);
         };
         if (g.x)
             fused_prologue<NPAD>(g, p, bars, threadIdx.x - kEpi0 * 32, btile0,
@@ -1211,7 +1240,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
                     const uint32_t dreg = tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD);
                     if (!kWide && g.B == 1) {
-                        // all of the region's columns in one batch of loads, one wait
+                        // all of the region's columns in one batch of loads, one wait; digit
+                        // Horner h = 4h + D_k (an odd a's lone last plane: 2h + D)
                         uint32_t dv[NPAD];
                         ld_tmem_cols<NPAD>(dreg, dv);
                         tmem_ld_wait();
@@ -1219,17 +1249,18 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                             te[3] = gtimer();
                             tcy[1] = clock64();
                         }
-                        unsigned long long h = 0ull - (unsigned long long)__float2uint_rn(__uint_as_float(dv[0]));
+                        unsigned long long h = d2i(dv[0]);
 #pragma unroll
                         for (int e = 1; e < NPAD; ++e) {
-                            const unsigned long long v = (unsigned long long)__float2uint_rn(__uint_as_float(dv[e]));
-                            h = (e < g.a) ? h + h + v : h;
+                            const unsigned long long v = d2i(dv[e]);
+                            const int sh = (e == nd - 1 && (g.a & 1)) ? 1 : 2;
+                            h = (e < nd) ? (h << sh) + v : h;
                         }
                         tot1 += h * wr;
                     } else if (plane_sums_dispatch<NPAD>(g.a, dreg, nb, m, s_tot_s, wr, r == 0)) {
                     } else {
-                        // any other a: per batch column, serial Horner; wide: 32 columns per batch
-                        // of loads
+                        // any other a: per batch column, serial digit Horner; wide: 32 columns
+                        // per batch of loads
                         constexpr int kCG = kWide ? 32 : NPAD;
                         unsigned long long h = 0;
                         int j = 0, bc = 0;
@@ -1245,10 +1276,10 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
 #pragma unroll
                             for (int e = 0; e < kCG; ++e) {
                                 if (bc < nb) {
-                                    const unsigned long long v =
-                                        (unsigned long long)__float2uint_rn(__uint_as_float(dv[e]));
-                                    h = j == 0 ? 0ull - v : h + h + v;
-                                    if (++j == g.a) {
+                                    const unsigned long long v = d2i(dv[e]);
+                                    const int sh = (j == nd - 1 && (g.a & 1)) ? 1 : 2;
+                                    h = j == 0 ? v : (h << sh) + v;
+                                    if (++j == nd) {
                                         const uint32_t sa = s_tot_s + (uint32_t)(bc * kTcRows + m) * 8u;
                                         const unsigned long long t = h * wr;
                                         st_shared_u64(sa, r == 0 ? t : t + ld_shared_u64(sa));
@@ -1282,8 +1313,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     if (!kWide && g.B == 1)
                         finish_tile_row(0, row, tot1);
                     else
-                        finish_cols(b0, nb, row,
-                                    [&](int b) { return ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u); });
+                        finish_cols(b0, nb, row);
                 } else {
                     if (!kWide && g.B == 1) {
                         red_add_u64(ab, tot1);
@@ -1307,8 +1337,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         asm volatile("bar.sync 1, 128;" ::: "memory");
                         if (bars.fin_tile >= 0) {
                             const int64_t row = (int64_t)rt * kTcRows + m;
-                            finish_cols(b0, nb, row, [&](int b) { return __ldcg(ab + b * kTcRows); });
-                            for (int b = 0; b < nb; ++b) ab[b * kTcRows] = 0;   // leave the sums zero
+                            finish_from_accbuf(b0, nb, row, ab);
                             if (ew == 0 && lane == 0) g.counters[slot] = 0;
                         }
                     }
@@ -1347,8 +1376,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         for (long long rt = blockIdx.x; rt < p.tiles; rt += G) {
             const int64_t row = rt * kTcRows + m;
             unsigned long long* ab = g.accbuf + rt * g.B * kTcRows + m;
-            finish_cols(0, (int)g.B, row, [&](int b) { return __ldcg(ab + b * kTcRows); });
-            for (int b = 0; b < g.B; ++b) ab[b * kTcRows] = 0;   // every call leaves the sums zero
+            finish_from_accbuf(0, (int)g.B, row, ab);                // (every call leaves the sums zero)
         }
         }   // !p.stat
         if (g.nranks) {
@@ -1455,7 +1483,7 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
 {
     const bool wide = npad > kTcMaxN;
     if (npad <= 0 || g.kwords <= 0 || g.R <= 0 || g.B <= 0 || g.L > 16) return false;
-    if (wide ? (npad != kTcWideN || g.x || g.nranks || g.bs < 1 || (int64_t)g.bs * g.a > npad)
+    if (wide ? (npad != kTcWideN || g.x || g.nranks || g.bs < 1 || (int64_t)g.bs * act_digits(g.a) > npad)
              : (g.B > kTcMaxB))
         return false;
     p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
@@ -1464,8 +1492,9 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     p.slices = wide ? (int)((g.B + g.bs - 1) / g.bs) : 1;
     p.units = (long long)p.slices * p.tiles * p.chunks;
     if (p.units >= (1ll << 30)) return false;                  // int unit indices in the kernel
-    // exact f32 accumulation: a group of G layers sums to < K * 2^G <= 2^24
-    int G = 24 - ceil_log2_i(g.kwords * 32);
+    // exact f32 accumulation: per pass and column |(2 hi + lo) d| <= 9 (signed activation
+    // digits, |d| <= 3), so a group of G layers sums to |D| < 3 K 2^G <= 2^24
+    int G = 24 - ceil_log2_i(3 * g.kwords * 32);
     if (G > 15) G = 15;                           // SFB exponents 0..13 fit the 64-column SF area
     p.Gp = G / 2;
     if (p.Gp < 1) return false;

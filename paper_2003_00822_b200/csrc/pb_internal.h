@@ -11,7 +11,8 @@ namespace pb {
 constexpr int kMaxSplit = 64;        // activation kernel CTAs per batch column (max)
 constexpr size_t kAlign = 256;
 constexpr int kTcRows = 128;         // tensor engine row tile (MMA M)
-constexpr int kTcMaxN = 64;          // tensor engine: a * batch <= 64 per launch (MMA N padded to 8/16/32/64)
+constexpr int kTcMaxN = 64;          // tensor engine narrow mode: ceil(a/2) * batch <= 64 digit columns per
+                                     // launch (MMA N padded to 8/16/32/64)
 constexpr int kTcMaxB = 32;          // tensor engine: batch columns per launch
 constexpr int kTcWideN = 128;        // wide mode: MMA N = 128 plane columns per slice, every slice
                                      // of the batch in one launch (single-buffered accumulator)
@@ -19,27 +20,30 @@ constexpr int kMaxRanks = 8;         // pb_matmul_rowshard_p2p: ranks of one nod
 
 inline size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
 
-// MMA N (plane columns a*batch padded to a legal tcgen05 kind::mxf4 N for M = 128),
-// 0 when the tensor engine's operand tiles are not produced for this shape.
+// Activation digits per batch column: the a planes stacked in pairs (pb_common.cuh).
+inline int digits_of(int32_t a) { return (a + 1) / 2; }
+// MMA N (digit columns batch * ceil(a/2) padded to a legal tcgen05 kind::mxf4 N for M = 128),
+// 0 when the tensor engine's narrow operand tiles are not produced for this shape.
 inline int tc_npad(int64_t batch, int32_t a) {
-    const int64_t n = batch * a;
-    if (n <= 0 || n > kTcMaxN || batch > kTcMaxB) return 0;
+    const int64_t n = batch * digits_of(a);
+    if (a <= 0 || n <= 0 || n > kTcMaxN || batch > kTcMaxB) return 0;
     return n <= 8 ? 8 : (n <= 16 ? 16 : (n <= 32 ? 32 : 64));
 }
-// Batch columns per tensor-engine launch: the whole batch when it fits, else slices of
-// min(32, 64 / a) columns (pb_matmul / pb_linear run one fused launch per slice).
+// Batch columns per narrow tensor-engine launch: the whole batch when it fits, else slices of
+// min(32, 64 / ceil(a/2)) columns (pb_matmul / pb_linear run one fused launch per slice).
 inline int64_t tc_slice(int64_t batch, int32_t a) {
     if (tc_npad(batch, a) > 0 || a <= 0) return batch;
-    int64_t s = kTcMaxN / a;
+    int64_t s = kTcMaxN / digits_of(a);
     if (s > kTcMaxB) s = kTcMaxB;
     return s < 1 ? 1 : s;
 }
-
-// Wide mode (a*batch > 64, 8 <= a <= 32): batch columns per 128-column slice, else 0.
-// (a >= 8 keeps the per-slice epilogue sums, <= 16 x 1 KiB of SMEM, beside >= 4 weight stages.)
+// Wide mode (digit columns > 64): batch columns per 128-column slice (at most kTcWideB: the
+// per-slice epilogue sums, 1 KiB each, share SMEM with >= 4 weight stages), else 0.
+constexpr int kTcWideB = 16;
 inline int tc_wide_bs(int64_t batch, int32_t a) {
-    if (a < 8 || a > 32 || tc_npad(batch, a) > 0 || batch <= 0) return 0;
-    return kTcWideN / a;
+    if (a < 1 || a > 32 || tc_npad(batch, a) > 0 || batch <= 0) return 0;
+    const int bs = kTcWideN / digits_of(a);
+    return bs < kTcWideB ? bs : kTcWideB;
 }
 
 // Workspace carve-up (documented in pb.h, pb_workspace_bytes):
@@ -78,7 +82,7 @@ inline WsLayout ws_layout(int64_t batch, int64_t kwords, int32_t act_bits) {
     // partial-tile sums sized for the largest slice this act_bits can launch (not this batch's),
     // so calls of different batch sizes with the same act_bits can share one workspace: the
     // region every call expects zero on entry is the same for all of them
-    int64_t bs_max = act_bits > 0 ? kTcMaxN / act_bits : 1;
+    int64_t bs_max = act_bits > 0 ? kTcMaxN / digits_of(act_bits) : 1;
     if (bs_max > kTcMaxB) bs_max = kTcMaxB;
     if (bs_max < 1) bs_max = 1;
     if (bs_max < bs) bs_max = bs;
