@@ -864,7 +864,8 @@ size_t pb_lstm_seq_workspace_bytes(int64_t steps, int64_t batch, int64_t in_cols
     const int64_t cols = steps * batch > batch ? steps * batch : batch;
     return pb::align_up(pb_workspace_bytes(cols, k, act_bits)) +
            pb::align_up(sizeof(float) * (size_t)cols * 4 * (size_t)hidden) +
-           2 * pb::align_up(sizeof(float) * (size_t)batch * (size_t)hidden);
+           2 * pb::align_up(sizeof(float) * (size_t)batch * (size_t)hidden) +
+           pb::align_up(sizeof(unsigned long long) * 2 * pb::kLstmMaxB);   // persistent kernel: max|h| slots
 }
 
 pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float* h0, const float* c0,
@@ -899,6 +900,48 @@ pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float*
     if ((st = act_and_gemm(x, cols, w_ih, k_used_ih, act_bits, PB_ACT_AUTO, bias, PB_FN_NONE, gx, nullptr, ws,
                            act_ws, s)) != PB_OK)
         return st;
+    // 2. the recurrence: all T timesteps in ONE persistent tensor-engine launch (a grid barrier
+    //    per timestep, pb_lstm_tc.cu) when W_hh's units fit the SMs at once; PB_LSTM_PERSIST=0
+    //    selects the per-timestep launches below
+    const char* pev = getenv("PB_LSTM_PERSIST");      // comparison knob, read per call
+    const int persist_env = pev ? atoi(pev) : 1;
+    if (persist_env && g_engine != PB_ENGINE_POPC) {
+        pb::LstmArgs la{};
+        la.bits = w_hh->bits;
+        la.R = w_hh->rows;
+        la.kwords = w_hh->kwords;
+        la.H = H;
+        la.L = w_hh->layers;
+        la.offset = w_hh->offset;
+        la.k_used = k_used_hh;
+        la.a = act_bits;
+        la.scale = w_hh->scale;
+        la.B = (int)batch;
+        la.T = (int)steps;
+        la.h0 = h0;
+        la.c0 = c0;
+        la.gx = gx;
+        la.h_seq = h_seq;
+        la.c_seq = c_seq;
+        la.c_last = c_last;
+        la.cbuf0 = cb[0];
+        la.cbuf1 = cb[1];
+        const pb::WsLayout lw = pb::ws_layout(cols, k > 0 ? pb_kwords(k) : 0, act_bits);
+        la.counters = reinterpret_cast<int*>(base + lw.off_count);
+        la.gbar = la.counters + pb::kMaxTiles;
+        la.accbuf = reinterpret_cast<unsigned long long*>(base + lw.off_slots);
+        la.tl = pb::debug_tl();
+        la.maxslot = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(cb[1]) +
+                                                           pb::align_up(sizeof(float) * (size_t)batch * (size_t)H));
+        const bool room = (lw.npad || lw.wbs) &&
+                          (size_t)((la.R + pb::kTcRows - 1) / pb::kTcRows) * (size_t)batch * pb::kTcRows * 8 <=
+                              lw.off_f - lw.off_slots;
+        if (room && H % 4 == 0 && batch <= pb::kLstmMaxB && pb::lstm_persist_supported(la)) {
+            cudaError_t e = pb::launch_lstm_persist(la, static_cast<cudaStream_t>(s));
+            if (e != cudaSuccess) return cuda_fail(e, "persistent lstm launch");
+            return PB_OK;
+        }
+    }
     // 2. per timestep: W_hh h_t + gx[t], then the cell -- fused into the tensor engine's
     //    finalisation when the shape allows (one launch for batch 1; planes kernel + GEMM when
     //    a batch > 1 fits one tensor-engine launch: measured faster than the fused prologue's

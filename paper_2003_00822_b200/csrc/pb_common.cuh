@@ -131,9 +131,8 @@ __device__ __forceinline__ void put_b_operand_smem(uint32_t tile_s, int npad, in
 // Warp-collective; returns whether this lane writes digit lane / 2.
 __device__ __forceinline__ bool digit_of_lane(uint32_t mine, int lane, int a, uint4& v) {
     const uint32_t partner = __shfl_down_sync(0xffffffffu, mine, 1);
-    if ((lane & 1) || lane >= a) return false;
-    v = digit_regs(mine, partner, lane == 0 ? ~0u : 0u, lane == a - 1 ? ~0u : 0u);
-    return true;
+    v = digit_regs(mine, partner, lane == 0 ? ~0u : 0u, lane == a - 1 ? ~0u : 0u);   // branch-free
+    return !(lane & 1) && lane < a;
 }
 
 // Next diagnostics-timeline record (pb_internal.h, pb_debug_timeline) or null when full.

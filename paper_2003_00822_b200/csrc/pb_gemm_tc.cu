@@ -475,23 +475,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     }
     const uint32_t tmem = warp == 0 ? 0u : bars.tmem_base;
     if (warp >= kConv0 && warp < kConv0 + 4) {
-        // E8M0 block scale factors: columns 0..3 = 1.0 (SFA), columns 4(1+s)..4(1+s)+3 = 2^s
-        // (SFB of passes with in-group weight 2^s); every byte of a column holds the same value
-#pragma unroll
-        for (int blk = 0; blk < 4; ++blk) {
-            uint32_t v[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const int col = blk * 16 + c, sidx = col / 4;   // sidx 0 = SFA, 1 + s = 2^s
-                v[c] = 0x01010101u * (uint32_t)(127 + (sidx == 0 ? 0 : sidx - 1));
-            }
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-                    tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(p.sf_col + blk * 16)),
-                "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-                "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-                : "memory");
-        }
+        store_scale_factors(tmem, warp, p.sf_col);
         tmem_st_wait();
     }
     if (warp != 0) {
@@ -741,18 +725,18 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
                     tc_fence_after();
                     const int kind = stored_pair ? (use_lo ? 0 : 1) : 2;
-                    const uint32_t xm = ps == 0 ? (stored_pair ? 0xAAAAAAAAu : 0xFFFFFFFFu) : 0u;
+                    const int sgn = ps == 0 ? (g.offset ? 2 : 1) : 0;   // the sign layer's pass: signed nibbles
                     const uint32_t t0 = wtile_s + (uint32_t)st0 * kWTileBytes;
                     const uint32_t t1 = wtile_s + (uint32_t)st1 * kWTileBytes;
                     const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
                     uint64_t* r0 = &bars.w_empty[st0];
                     uint64_t* r1 = &bars.w_empty[st1];
                     if (kind == 0)
-                        convert_pass<0>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
+                        convert_pass<0>(t0, t1, swz, dst, sgn, p.dbg, r0, r1, lane);
                     else if (kind == 1)
-                        convert_pass<1>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
+                        convert_pass<1>(t0, t1, swz, dst, sgn, p.dbg, r0, r1, lane);
                     else
-                        convert_pass<2>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
+                        convert_pass<2>(t0, t1, swz, dst, sgn, p.dbg, r0, r1, lane);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
                     tc += ntile;
                     converted = true;
@@ -776,7 +760,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const int m = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer; + the midpoint offset
-        const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0) + g.mid;
+        // the midpoint offset 2^(L-k_used-1) sum_c x_q (pb_matmul_ex); the sign layer carries its
+        // own negative weight (signed nibbles), so nothing else needs sum_c x_q
+        const unsigned long long o_corr = g.mid;
         bool have_xsum = false;
         const int pt = threadIdx.x - kEpi0 * 32;      // 0..127
         const int nd = act_digits(g.a);               // activation digits per batch column
@@ -814,7 +800,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // a5: y = dequant(acc) (+ bias, + y when accumulating), then fn -- or, in cell mode
         // (pb_lstm_seq), the LSTM cell over the 4 gate rows of a hidden unit (lanes 4j..4j+3)
         auto preact = [&](int b, int64_t row, unsigned long long t) -> float {
-            t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
+            if (o_corr) t += o_corr * xsum_of(b);
             const long long accv = (long long)t;
             const int64_t o = (int64_t)b * g.R + row;
             if (g.acc) g.acc[o] = accv;

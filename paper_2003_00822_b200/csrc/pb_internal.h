@@ -159,6 +159,34 @@ struct GemmArgs {
     unsigned long long* local_ctr;
 };
 
+// Persistent LSTM recurrence (pb_lstm_tc.cu): all T timesteps of
+// h_{t+1}, c_{t+1} = cell(gx[t] + W_hh h_t, c_t) in one launch, one CTA per (row tile,
+// K-chunk) unit of W_hh, a grid barrier per timestep.
+constexpr int kLstmMaxB = 32;        // batch columns (digit columns B * ceil(a/2) <= 128)
+struct LstmArgs {
+    const uint32_t* bits;   // W_hh [L][4H][kwords], gate-interleaved rows (row 4k + gate)
+    int64_t R, kwords, H;   // R = 4H
+    int L, offset, k_used, a;
+    double scale;
+    int B, T;
+    const float* h0;        // [B][H]
+    const float* c0;        // [B][H]
+    const float* gx;        // [T][B][4H]: W_ih x_t + bias (hoisted), gate-interleaved
+    float* h_seq;           // [T][B][H]
+    float* c_seq;           // [T][B][H] or null
+    float* c_last;          // [B][H]
+    float* cbuf0;           // [B][H] x 2 ping-pong c_t when c_seq is null
+    float* cbuf1;
+    unsigned long long* accbuf;   // [tiles][B][128] exact split-tile sums, zero between calls
+    int* counters;                // [tiles], zero between calls
+    int* gbar;                    // monotonic grid-barrier counter (+2^20 per timestep)
+    unsigned long long* maxslot;  // [2][kLstmMaxB] epoch-tagged max|h| (zero-filled once, never reset)
+    long long* tl;                // diagnostics timeline (PB_TC_DEBUG=6) or null
+};
+int lstm_persist_npad(int64_t batch, int32_t a);
+bool lstm_persist_supported(const LstmArgs& g);
+cudaError_t launch_lstm_persist(const LstmArgs& g, cudaStream_t s);
+
 // Diagnostics timeline (PB_TC_DEBUG=6): device log, [0] = record counter,
 // records of 10 int64 from index 10; null when off.
 constexpr long long kTlRecords = 1 << 16;

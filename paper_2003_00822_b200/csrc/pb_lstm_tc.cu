@@ -1,0 +1,633 @@
+// pb_lstm_tc.cu -- the LSTM recurrence as ONE persistent tensor-engine kernel (SURVEY §8(f)
+// f1): every timestep's 4-gate matvec W_hh h_t ("replace each linear layer
+// ... LSTM" with the bitlayer product) plus the cell, with a grid barrier per timestep
+// instead of a launch.
+//
+// The input projection W_ih x_t + b of all T timesteps is one batched call before this
+// kernel (pb_lstm_seq); here gx[t] is added to the recurrent pre-activations.  Per timestep
+// (Alg. 2 on h_t):
+//   a1-a2  every CTA reads h_t (B x H floats, L2): max|h_t[b,:]| -> f_b (reading G8),
+//          sum_c x_q over all H, and the activation digits of its own K-chunk straight into
+//          the MMA's B operand in SMEM (ballot transpose, pb_common.cuh);
+//   a3-a4  tcgen05.mma kind::mxf4 (two weight bitlayers per nibble, as pb_gemm_tc.cu) over
+//          the CTA's unit = 128 gate rows x 1024 columns, accumulated exactly in TMEM;
+//   a5     the unit's exact int64 row sums; a tile split over several CTAs (K > 1024) is
+//          summed exactly (red.add) and finished by the contributor that completes it:
+//          dequant (G13) + gx[t] -> the four gates of 32 hidden units (gate-interleaved rows,
+//          lanes 4j..4j+3) -> c' = s(f) c + s(i) tanh(g), h' = s(o) tanh(c') (reading G15);
+//   then one grid barrier (monotonic counter, pb_tc_device.cuh) publishes h_{t+1}.
+// The weights do not depend on h: warp 0 streams the unit's weight tiles through the TMA ring
+// and the converters build the A operand in TMEM for the next timestep while this one waits
+// on its barrier, so a timestep costs the barrier, the h read and the MMAs -- not a launch.
+//
+// One CTA per unit (tiles x chunks <= #SMs, all co-resident): 128 CTAs for H = 2048.
+// Warp roles (480 threads): 0 TMA producer, 1 TMEM allocator + MMA issuer, 2 idle after setup,
+// 3..10 converters (two h-sets of 4), 11..14 per-step prologue + epilogue.
+#include <cuda.h>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <mutex>
+
+#include "pb_common.cuh"
+#include "pb_internal.h"
+#include "pb_tc_device.cuh"
+
+namespace pb {
+namespace {
+
+constexpr int kConvWarps = 8;
+constexpr int kConv0 = 3;
+constexpr int kEpi0 = kConv0 + kConvWarps;
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 32 * (kEpi0 + kEpiWarps);
+constexpr int kMaxSlots = 4;
+constexpr int kMaxWStages = 16;
+constexpr uint32_t kHdrBytes = 4096;
+
+struct LBars {
+    uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
+    uint64_t w_full[kMaxWStages], w_empty[kMaxWStages];
+    uint64_t b_full, d_full, d_empty, h_full, h_empty;
+    uint64_t red_full;                         // cluster leader: the other chunks' partial sums are in
+    uint64_t gx_full[2];                       // step t's gx rows of the tile are in SMEM (by t & 1: warp 2
+                                               // runs one step ahead, a single barrier would overrun)
+    unsigned long long epoch0;                 // barrier instance of this call's step 0
+    uint32_t tmem_base;
+    int fin;                                   // this step: the CTA completed its tile (1) or not
+    float red[kEpiWarps][kLstmMaxB];           // per-warp partial max|h[b,:]|
+    int f[2][kLstmMaxB];                       // f_b of step t at [t & 1]
+    double sc[2][kLstmMaxB];                   // s_w 2^-f_b
+    float scl[2][kLstmMaxB];                   // 2^f_b as fp32 (the cast's fast path)
+};
+static_assert(sizeof(LBars) <= kHdrBytes, "LBars must fit the SMEM header");
+
+// Cluster (DSMEM) helpers: the CTAs of one cluster are the K-chunks of one row tile.
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_u64(uint32_t addr, unsigned long long v) {
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nWAITC_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct LPlan {
+    int tiles, chunks;
+    int slots, sf_col, d_col, wstages;
+    int passes, Gp, regions;
+};
+
+template <int NPAD>
+__global__ void __launch_bounds__(kThreads, 1)
+lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUtensorMap pmap,
+                    const __grid_constant__ CUtensorMap smap)
+{
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    LBars& bars = *reinterpret_cast<LBars*>(smem);
+    constexpr uint32_t kBTile = NPAD * 32;
+    constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;
+    constexpr bool kWide = NPAD > kTcMaxN;
+    uint8_t* wtile0 = smem + kHdrBytes;
+    uint8_t* bstage = wtile0 + p.wstages * kWTileBytes;
+    const uint32_t s_tot_s = smem_u32(bstage + kBStage);       // [b][128] u64 (B > 1)
+    uint8_t* hbuf = bstage + kBStage + (size_t)g.B * kTcRows * 8;  // [b][1024] fp32: the K-chunk of h_t
+    const uint32_t redbuf_s = smem_u32(hbuf + (size_t)g.B * kChunkWords * 32 * 4);   // [chunks-1][b][128] u64
+    float* gxbuf = reinterpret_cast<float*>(hbuf + (size_t)g.B * kChunkWords * 32 * 4 +
+                                            (size_t)(p.chunks - 1) * g.B * kTcRows * 8);   // [2][b][128] fp32
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rt = blockIdx.x / p.chunks, kc = blockIdx.x - rt * p.chunks;
+    const int T = g.T;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.slots; ++s) {
+            mbar_init(&bars.a_full[s], 4);
+            mbar_init(&bars.a_empty[s], 1);
+        }
+        for (int s = 0; s < p.wstages; ++s) {
+            mbar_init(&bars.w_full[s], 1);
+            mbar_init(&bars.w_empty[s], 4);
+        }
+        mbar_init(&bars.b_full, 1);
+        mbar_init(&bars.d_full, 1);
+        mbar_init(&bars.d_empty, kEpiWarps);
+        mbar_init(&bars.h_full, 2);                // the copies (expect_tx) + f_b of the step
+        mbar_init(&bars.h_empty, 1);
+        mbar_init(&bars.red_full, p.chunks > 1 ? p.chunks - 1 : 1);
+        mbar_init(&bars.gx_full[0], 1);
+        mbar_init(&bars.gx_full[1], 1);
+        fence_mbar_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&pmap) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&smap) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            smem_u32(&bars.tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync();                                // barrier inits visible to the cluster's CTAs
+    tc_fence_after();
+    const uint32_t tmem = bars.tmem_base;
+    if (warp >= kConv0 && warp < kConv0 + 4) {
+        store_scale_factors(tmem, warp, p.sf_col);
+        tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_trigger();
+
+    if (warp == 0) {
+        // ---------------------------------------------- weight tiles of this CTA's unit, every
+        // timestep (L2-resident after the first), as far ahead as the ring allows
+        int tc = 0;
+        for (int t = 0; t < T; ++t)
+            for (int ps = 0; ps < p.passes; ++ps) {
+                const bool stored_pair = 2 * ps + 1 < g.L;
+                for (int h = 0; h < (stored_pair ? 2 : 1); ++h, ++tc) {
+                    const int st = tc % p.wstages;
+                    mbar_wait(&bars.w_empty[st], (uint32_t)(((tc / p.wstages) & 1) ^ 1));
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(&bars.w_full[st], kWTileBytes);
+                        if (stored_pair)
+                            tma_load_3d(wtile0 + st * kWTileBytes, &pmap, kc * 2 * kChunkWords + h * kChunkWords,
+                                        rt * kTcRows, ps, &bars.w_full[st]);
+                        else
+                            tma_load_3d(wtile0 + st * kWTileBytes, &smap, kc * kChunkWords, rt * kTcRows, 0,
+                                        &bars.w_full[st]);
+                    }
+                    __syncwarp();
+                }
+            }
+    } else if (warp == 1) {
+        // ---------------------------------------------- MMA issuer
+        const uint32_t idesc = mxf4_idesc(NPAD);
+        const uint32_t sfa = tmem + p.sf_col;
+        const uint64_t bdesc0 = b_desc(smem_u32(bstage));
+        uint32_t slot = 0, phase = 0;
+        for (int t = 0; t < T; ++t) {
+            mbar_wait(&bars.b_full, (uint32_t)(t & 1));                 // h_t's digits are in SMEM
+            if (t > 0) mbar_wait(&bars.d_empty, (uint32_t)((t - 1) & 1));   // D(t-1) drained
+            tc_fence_after();
+            for (int ps = 0; ps < p.passes; ++ps) {
+                int region, sexp;
+                bool first;
+                pass_region_g(p.Gp, p.passes, g.k_used, ps, region, sexp, first);
+                const uint32_t dcol = tmem + (uint32_t)(p.d_col + region * NPAD);
+                const uint32_t sfb = tmem + (uint32_t)(p.sf_col + 4 * (1 + sexp));
+                mbar_wait(&bars.a_full[slot], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t a0 = tmem + slot * 128;
+#pragma unroll
+                    for (int uu = 0; uu < 16; ++uu)
+                        tc_mma(dcol, a0 + 8 * uu, bdesc0 + uu * (kBTile / 16), idesc, (uu == 0 && first) ? 0u : 1u,
+                               sfa, sfb);
+                    tc_commit(&bars.a_empty[slot]);
+                }
+                __syncwarp();
+                if (++slot == (uint32_t)p.slots) {
+                    slot = 0;
+                    phase ^= 1;
+                }
+            }
+            if (elect_one()) tc_commit(&bars.d_full);
+            __syncwarp();
+        }
+    } else if (warp >= kConv0 && warp < kEpi0) {
+        // ---------------------------------------------- converters (as pb_gemm_tc.cu): pass pc of
+        // the whole run goes to h-set pc & 1 and A slot pc % slots
+        const int cw = warp - kConv0;
+        const int h = cw >> 2;
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const uint32_t wtile_s = smem_u32(wtile0) + (uint32_t)m * 128;
+        const uint32_t swz = (uint32_t)(m & 7);
+        int tc = 0, pc = 0;
+        int slot = h % p.slots, sphase = (h / p.slots) & 1;
+        int pend_slot = -1;
+        auto publish = [&]() {
+            if (pend_slot >= 0) {
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bars.a_full[pend_slot]);
+                pend_slot = -1;
+            }
+        };
+        for (int t = 0; t < T; ++t)
+            for (int ps = 0; ps < p.passes; ++ps, ++pc) {
+                const bool stored_pair = 2 * ps + 1 < g.L;
+                const bool use_lo = 2 * ps + 1 < g.k_used;
+                const int ntile = stored_pair ? 2 : 1;
+                if ((pc & 1) != h) {
+                    tc += ntile;
+                    continue;
+                }
+                const int st0 = tc % p.wstages, st1 = (tc + ntile - 1) % p.wstages;
+                mbar_wait(&bars.w_full[st0], (uint32_t)((tc / p.wstages) & 1));
+                if (stored_pair) mbar_wait(&bars.w_full[st1], (uint32_t)(((tc + 1) / p.wstages) & 1));
+                publish();
+                mbar_wait(&bars.a_empty[slot], (uint32_t)(sphase ^ 1));
+                tc_fence_after();
+                const int kind = stored_pair ? (use_lo ? 0 : 1) : 2;
+                const int sgn = ps == 0 ? (g.offset ? 2 : 1) : 0;   // the sign layer's pass: signed nibbles
+                const uint32_t t0 = wtile_s + (uint32_t)st0 * kWTileBytes;
+                const uint32_t t1 = wtile_s + (uint32_t)st1 * kWTileBytes;
+                const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
+                if (kind == 0)
+                    convert_pass<0>(t0, t1, swz, dst, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                else if (kind == 1)
+                    convert_pass<1>(t0, t1, swz, dst, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                else
+                    convert_pass<2>(t0, t1, swz, dst, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                tc += ntile;
+                pend_slot = slot;
+                slot += 2;
+                while (slot >= p.slots) {
+                    slot -= p.slots;
+                    sphase ^= 1;
+                }
+            }
+        publish();
+    } else if (warp == 2) {
+        // ---------------------------------------------- step gate: once h_t is complete on every
+        // CTA (grid barrier of step t-1), copy this CTA's K-chunk of h_t (B rows of <= 1024
+        // floats) into SMEM for the prologue (1-D bulk copies completing on h_full)
+        pdl_wait();
+        unsigned long long gbase = 0;
+        if (lane == 0) gbase = grid_base(g.gbar);
+        const int H = (int)g.H;
+        const int c0 = kc * kChunkWords * 32;
+        const int ncol = H - c0 < kChunkWords * 32 ? H - c0 : kChunkWords * 32;
+        const int64_t r0 = (int64_t)rt * kTcRows;
+        const int nrow = g.R - r0 < kTcRows ? (int)(g.R - r0) : kTcRows;
+        for (int t = 0; t < T; ++t) {
+            if (t > 0) mbar_wait(&bars.h_empty, (uint32_t)((t - 1) & 1));   // the prologue read h_{t-1}
+            if (lane == 0 && kc == 0) {
+                // the tile's rows of gx[t] (no dependence on h): in flight while the step waits
+                mbar_arrive_expect_tx(&bars.gx_full[t & 1], (uint32_t)(g.B * nrow * 4));
+                for (int b = 0; b < g.B; ++b)
+                    bulk_g2s(gxbuf + ((t & 1) * g.B + b) * kTcRows, g.gx + ((int64_t)t * g.B + b) * g.R + r0,
+                             (uint32_t)(nrow * 4), &bars.gx_full[t & 1]);
+            }
+            if (lane == 0) {
+                if (t > 0) {
+                    const unsigned long long* c = reinterpret_cast<const unsigned long long*>(g.gbar);
+                    while (ld_acquire_gpu_u64(c) < gbase + (unsigned long long)t * kGridStride) {
+                    }
+                    asm volatile("fence.proxy.async.global;" ::: "memory");   // generic h stores -> bulk reads
+                }
+                const float* x = t == 0 ? g.h0 : g.h_seq + (int64_t)(t - 1) * g.B * H;
+                mbar_arrive_expect_tx(&bars.h_full, (uint32_t)(g.B * ncol * 4));
+                for (int b = 0; b < g.B; ++b)
+                    bulk_g2s(hbuf + (size_t)b * kChunkWords * 32 * 4, x + (int64_t)b * H + c0, (uint32_t)(ncol * 4),
+                             &bars.h_full);
+            }
+            __syncwarp();
+            // f_b of step t > 0 from the maxima the producers of h_t published (epoch-tagged
+            // atomicMax slots, pb_internal.h), while the copies fly (step 0: the prologue reads h0)
+            if (t > 0 && lane < g.B) {
+                const unsigned long long v = __ldcg(g.maxslot + ((t & 1) * kLstmMaxB + lane));
+                const int f = act_frac_of(__uint_as_float((uint32_t)v), g.a);
+                bars.f[t & 1][lane] = f;
+                bars.sc[t & 1][lane] = col_scale(g.scale, f);
+                bars.scl[t & 1][lane] = (f >= -126 && f <= 127) ? __int_as_float((127 + f) << 23) : 0.f;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars.h_full);
+        }
+    } else if (warp >= kEpi0) {
+        // ---------------------------------------------- per-step prologue + epilogue (128 threads)
+        const int pt = threadIdx.x - kEpi0 * 32, ew = pt >> 5;
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const int B = g.B, H = (int)g.H, a = g.a;
+        const int nd = act_digits(a);
+        const int64_t R = g.R;
+        const int64_t row = (int64_t)rt * kTcRows + m;
+        const uint32_t bstage_s = smem_u32(bstage);
+        const uint32_t hbuf_s = smem_u32(hbuf);
+        pdl_wait();                                  // h0 / gx come from earlier kernels
+        if (pt == 0) bars.epoch0 = grid_base(g.gbar) / kGridStride;
+        for (int t = 0; t < T; ++t) {
+            // ---- a1: f_b from max|h_t[b,:]| (reading G8).  Step 0 reads all of h0; h_t for t > 0
+            //      comes with its maxima, published by the CTAs that produced it (epoch-tagged
+            //      atomicMax slots: (barrier instance << 32) | float bits, never reset)
+            if (t == 0) {
+                for (int b = 0; b < B; ++b) {
+                    const float4* x4 = reinterpret_cast<const float4*>(g.h0 + (int64_t)b * H);
+                    float mx = 0.f;
+                    for (int c = pt; c < H / 4; c += 128) {
+                        const float4 v = __ldcg(x4 + c);
+                        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+                    }
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                    if (lane == 0) bars.red[ew][b] = mx;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (pt < B) {
+                    float mx = bars.red[0][pt];
+#pragma unroll
+                    for (int w = 1; w < kEpiWarps; ++w) mx = fmaxf(mx, bars.red[w][pt]);
+                    bars.f[0][pt] = act_frac_of(mx, a);
+                    bars.sc[0][pt] = col_scale(g.scale, bars.f[0][pt]);
+                    const int f = bars.f[0][pt];
+                    bars.scl[0][pt] = (f >= -126 && f <= 127) ? __int_as_float((127 + f) << 23) : 0.f;
+                }
+            }
+            long long tm[6] = {0, 0, 0, 0, 0, 0};
+            if (g.tl) tm[0] = gtimer();
+            if (t == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(&bars.h_full, (uint32_t)(t & 1));
+            if (g.tl) tm[1] = gtimer();
+            const int par = t & 1;
+            // ---- a1-a2: the digits of this CTA's chunk into the B operand: items (b, word), each
+            //      warp 8 items at a time (independent ballot chains), values from the SMEM copy
+            const int nit = B * kChunkWords;
+            // the exact fp32 cast of act_cast (pb_common.cuh) when every f_b of the step is in range
+            bool fast = a <= 24;
+            for (int b = 0; b < B && fast; ++b) fast = bars.scl[par][b] != 0.f;
+            const float lim = (float)(1 << ((a <= 24 ? a : 24) - 1));
+            for (int k0 = 0; ew + kEpiWarps * k0 < nit; k0 += 8) {
+                uint32_t u[8], mm[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int it = ew + kEpiWarps * (k0 + k);
+                    const int b = it / kChunkWords, cl = (it - b * kChunkWords) * 32 + lane;
+                    float v = 0.f;
+                    if (it < nit && (int64_t)kc * kChunkWords * 32 + cl < H)
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(hbuf_s + (uint32_t)((b * kChunkWords * 32 + cl) * 4)));
+                    if (fast) {
+                        float tq = v * bars.scl[par][b];
+                        tq = fminf(fmaxf(tq, -lim), lim - 1.0f);
+                        u[k] = (uint32_t)__float2int_rz(tq);
+                    } else {
+                        u[k] = it < nit ? (uint32_t)act_cast(v, bars.f[par][b], a) : 0u;
+                    }
+                    mm[k] = 0;
+                }
+#pragma unroll 1
+                for (int j = 0; j < a; ++j) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const uint32_t w = __ballot_sync(0xffffffffu, (u[k] >> (a - 1 - j)) & 1u);
+                        if (lane == j) mm[k] = w;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int it = ew + kEpiWarps * (k0 + k);
+                    if (it < nit) {                               // warp-uniform
+                        const int b = it / kChunkWords, wl = it - b * kChunkWords;
+                        uint4 dv;
+                        if (digit_of_lane(mm[k], lane, a, dv))
+                            put_b_operand_smem(bstage_s, NPAD, wl, b * nd + (lane >> 1), dv);
+                        if (b == B - 1)
+                            for (int n = B * nd + lane; n < NPAD; n += 32)
+                                put_b_operand_smem(bstage_s, NPAD, wl, n, make_uint4(0, 0, 0, 0));
+                    }
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (pt == 0) {
+                mbar_arrive(&bars.b_full);
+                mbar_arrive(&bars.h_empty);
+            }
+            if (g.tl) tm[2] = gtimer();
+            // ---- a3-a4 done: drain D into exact per-row sums per batch column (s_tot)
+            mbar_wait(&bars.d_full, (uint32_t)(t & 1));
+            tc_fence_after();
+            if (g.tl) tm[3] = gtimer();
+            unsigned long long tot1 = 0;
+            for (int r = 0; r < p.regions; ++r) {
+                int last = (r + 1) * p.Gp - 1;
+                if (last > p.passes - 1) last = p.passes - 1;
+                const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
+                const uint32_t dreg = tmem + lane_off + (uint32_t)(p.d_col + r * NPAD);
+                if (!kWide && B == 1) {
+                    uint32_t dv[NPAD];
+                    ld_tmem_cols<NPAD>(dreg, dv);
+                    tmem_ld_wait();
+                    unsigned long long hh = d2i(dv[0]);
+#pragma unroll
+                    for (int e = 1; e < NPAD; ++e) {
+                        const int sh = (e == nd - 1 && (a & 1)) ? 1 : 2;
+                        hh = (e < nd) ? (hh << sh) + d2i(dv[e]) : hh;
+                    }
+                    tot1 += hh * wr;
+                } else if (!plane_sums_dispatch<NPAD>(a, dreg, B, m, s_tot_s, wr, r == 0)) {
+                    // any other a: serial digit Horner per batch column
+                    constexpr int kCG = NPAD < 32 ? NPAD : 32;
+                    unsigned long long hh = 0;
+                    int j = 0, bc = 0;
+                    for (int c0 = 0; c0 < NPAD && bc < B; c0 += kCG) {
+                        uint32_t dv[kCG];
+                        ld_tmem_cols<kCG>(dreg + (uint32_t)c0, dv);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < kCG; ++e)
+                            if (bc < B) {
+                                const int sh = (j == nd - 1 && (a & 1)) ? 1 : 2;
+                                hh = j == 0 ? d2i(dv[e]) : (hh << sh) + d2i(dv[e]);
+                                if (++j == nd) {
+                                    const uint32_t sa = s_tot_s + (uint32_t)(bc * kTcRows + m) * 8u;
+                                    st_shared_u64(sa, r == 0 ? hh * wr : hh * wr + ld_shared_u64(sa));
+                                    j = 0;
+                                    ++bc;
+                                }
+                            }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars.d_empty);
+            auto tot_of = [&](int b) -> unsigned long long {
+                return (!kWide && B == 1) ? tot1 : ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u);
+            };
+            // ---- a5: a tile's K-chunks are the CTAs of one cluster: the others put their exact
+            //      partial sums into the leader's SMEM (DSMEM) and the leader finishes the tile
+            const bool finish = kc == 0;
+            if (!finish) {
+                const uint32_t rb = mapa_shared(redbuf_s + (uint32_t)(((kc - 1) * B * kTcRows + m) * 8), 0);
+                for (int b = 0; b < B; ++b) st_cluster_u64(rb + (uint32_t)(b * kTcRows * 8), tot_of(b));
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (pt == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&bars.red_full), 0));
+            } else if (p.chunks > 1) {
+                mbar_wait_cluster(&bars.red_full, (uint32_t)(t & 1));
+            }
+            if (finish) {
+                const float* c_in = t == 0 ? g.c0 : (g.c_seq ? g.c_seq + (int64_t)(t - 1) * B * H : (((t - 1) & 1) ? g.cbuf1 : g.cbuf0));
+                float* c_out = g.c_seq ? g.c_seq + (int64_t)t * B * H : (t == T - 1 ? g.c_last : ((t & 1) ? g.cbuf1 : g.cbuf0));
+                float* h_out = g.h_seq + (int64_t)t * B * H;
+                mbar_wait(&bars.gx_full[t & 1], (uint32_t)((t >> 1) & 1));
+                for (int b = 0; b < B; ++b) {
+                    unsigned long long tt = tot_of(b);
+                    for (int r = 1; r < p.chunks; ++r)
+                        tt += ld_shared_u64(redbuf_s + (uint32_t)((((r - 1) * B + b) * kTcRows + m) * 8));
+                    const float v = row < R ? dequant_sc((long long)tt, bars.sc[par][b]) + gxbuf[(par * B + b) * kTcRows + m] : 0.f;
+                    const int q0 = lane & ~3;
+                    const float gi = __shfl_sync(0xffffffffu, v, q0), gf = __shfl_sync(0xffffffffu, v, q0 + 1);
+                    const float gg = __shfl_sync(0xffffffffu, v, q0 + 2), go = __shfl_sync(0xffffffffu, v, q0 + 3);
+                    float hn = 0.f;
+                    if ((lane & 3) == 0 && row < R) {
+                        const int64_t i = (int64_t)b * H + (row >> 2);
+                        float cn;
+                        lstm_cell(gi, gf, gg, go, c_in[i], hn, cn);
+                        h_out[i] = hn;
+                        c_out[i] = cn;
+                        if (g.c_seq && t == T - 1) g.c_last[i] = cn;
+                    }
+                    // max|h_{t+1}[b,:]| over this warp's 8 hidden units -> step t+1's f_b
+                    float mh = fabsf(hn);
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+                    if (lane == 0 && t + 1 < T)
+                        atomicMax(g.maxslot + (((t + 1) & 1) * kLstmMaxB + b),
+                                  ((bars.epoch0 + (unsigned long long)t + 1) << 32) | __float_as_uint(mh));
+                }
+            }
+            // ---- publish h_{t+1}: every CTA arrives (the 128 threads' stores are ordered before
+            //      thread 0's release by bar.sync)
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (pt == 0) grid_arrive(g.gbar);
+            if (g.tl && pt == 0) {
+                long long* rr = tl_record(g.tl);
+                if (rr) {
+                    const long long rec[10] = {7, blockIdx.x, t, tm[0], tm[1], tm[2], tm[3], finish ? 1 : 0, gtimer(), 0};
+                    for (int k = 0; k < 10; ++k) rr[k] = rec[k];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync();                                // no CTA leaves while its SMEM may be written
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// SMEM besides the weight ring: header, B stage, per-row sums, the K-chunk of h_t, and the
+// leader's buffer for the other chunks' partial sums.
+uint32_t lstm_fixed_smem(int B, int npad, int chunks) {
+    return 1024 + kHdrBytes + (uint32_t)(kChunkWords / 2) * npad * 32 + (uint32_t)B * kTcRows * 8 +
+           (uint32_t)B * kChunkWords * 32 * 4 + (uint32_t)(chunks - 1) * B * kTcRows * 8 + 2u * B * kTcRows * 4;
+}
+
+bool make_lplan(const LstmArgs& g, int npad, int sms, LPlan& p)
+{
+    if (g.B < 1 || g.B > kLstmMaxB || g.T < 1 || g.L < 1 || g.L > 16 || g.H % 4 || g.R != 4 * g.H) return false;
+    if ((int64_t)g.B * act_digits(g.a) > npad) return false;
+    p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
+    p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
+    if ((int64_t)p.tiles * p.chunks > sms) return false;       // one unit per CTA, all co-resident
+    if (p.chunks > 8) return false;                             // a tile's chunks form one (portable) cluster
+    p.Gp = tc_group_passes(g.kwords);
+    if (p.Gp < 1) return false;
+    p.passes = (g.k_used + 1) / 2;
+    p.regions = (p.passes + p.Gp - 1) / p.Gp;
+    p.d_col = 512 - (p.regions * npad + 31) / 32 * 32;          // one accumulator set
+    p.sf_col = p.d_col - 64;
+    p.slots = p.sf_col / 128;
+    if (p.slots > kMaxSlots) p.slots = kMaxSlots;
+    if (p.slots < 2) return false;
+    p.wstages = (int)((kSmemMax - lstm_fixed_smem(g.B, npad, p.chunks)) / kWTileBytes);
+    if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
+    // >= 4: the two converter h-sets wait on the tiles of consecutive passes (2 tiles each); with
+    // fewer stages a parity wait could see a barrier two phases behind it
+    return p.wstages >= 4;
+}
+
+std::mutex g_lmu;
+bool g_lattr[64][5];
+
+template <int NPAD>
+cudaError_t launch_lt(const LstmArgs& g, cudaStream_t s)
+{
+    int dev = 0, sms = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+    LPlan p;
+    if (!make_lplan(g, NPAD, sms, p)) return cudaErrorNotSupported;
+    constexpr int ai = NPAD == 8 ? 0 : (NPAD == 16 ? 1 : (NPAD == 32 ? 2 : (NPAD == 64 ? 3 : 4)));
+    if (dev >= 0 && dev < 64 && !g_lattr[dev][ai]) {
+        std::lock_guard<std::mutex> lk(g_lmu);
+        e = cudaFuncSetAttribute(lstm_persist_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax);
+        if (e != cudaSuccess) return e;
+        g_lattr[dev][ai] = true;
+    }
+    GemmArgs ga{};
+    ga.bits = g.bits;
+    ga.R = g.R;
+    ga.kwords = g.kwords;
+    ga.L = g.L;
+    CUtensorMap pmap, smap;
+    if ((e = tc_weight_maps(ga, &pmap, &smap)) != cudaSuccess) return e;
+    const uint32_t smem = lstm_fixed_smem(g.B, NPAD, p.chunks) + (uint32_t)p.wstages * kWTileBytes;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.tiles * p.chunks), 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute la[2];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    la[1].id = cudaLaunchAttributeClusterDimension;             // a tile's K-chunks: one cluster
+    la[1].val.clusterDim.x = (unsigned)p.chunks;
+    la[1].val.clusterDim.y = 1;
+    la[1].val.clusterDim.z = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, lstm_persist_kernel<NPAD>, g, p, pmap, smap);
+}
+
+}  // namespace
+
+int lstm_persist_npad(int64_t batch, int32_t a) {
+    const int64_t n = batch * act_digits(a);
+    if (batch < 1 || batch > kLstmMaxB || a < 1 || a > 32 || n > kTcWideN) return 0;
+    return n <= 8 ? 8 : (n <= 16 ? 16 : (n <= 32 ? 32 : (n <= 64 ? 64 : kTcWideN)));
+}
+
+bool lstm_persist_supported(const LstmArgs& g)
+{
+    const int npad = lstm_persist_npad(g.B, g.a);
+    if (!npad) return false;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return false;
+    LPlan p;
+    return make_lplan(g, npad, sms, p);
+}
+
+cudaError_t launch_lstm_persist(const LstmArgs& g, cudaStream_t s)
+{
+    switch (lstm_persist_npad(g.B, g.a)) {
+        case 8: return launch_lt<8>(g, s);
+        case 16: return launch_lt<16>(g, s);
+        case 32: return launch_lt<32>(g, s);
+        case 64: return launch_lt<64>(g, s);
+        case kTcWideN: return launch_lt<kTcWideN>(g, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace pb

@@ -106,8 +106,9 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 //   KIND 1, upper layer only (k_used odd): 0.5*upper (the pass unit becomes |S_upper|):
 //       A_0 = (P0 >> 1) & 0x11111111, ..., A_3 = (P1 >> 3) & 0x11111111
 //   KIND 2, canonical single layer (the last layer of an odd L): A_r = (w >> r) & 0x11111111.
-// xm complements the sign layer (pass 0): 0xAAAAAAAA (its upper bits) for KIND 0/1, ~0 for
-// KIND 2, else 0; it folds into the mask op (a 3-input LOP3) at no cost.
+// The sign layer (pass 0) carries its negative weight S_0 in the nibble's sign bit
+// (sign_nibbles below), so every product is the signed integer term of sum_i S_i W_i and no
+// correction term remains.
 template <int KIND>
 __device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t xm, uint32_t (&v)[32]) {
     const uint32_t w[16] = {q[0].x, q[0].y, q[0].z, q[0].w, q[1].x, q[1].y, q[1].z, q[1].w,
@@ -137,6 +138,21 @@ __device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t xm, uint32
     }
 }
 
+// Pass 0 of a code: the sign layer's nibbles signed.  Per e2m1 nibble (bit 3 = sign):
+//   KIND 0, (upper = sign W_0, lower = W_1): -1.0 W_0 + 0.5 W_1 in {0, 0.5, -1, -0.5}
+//     = 0000 / 0001 / 1010 / 1001: bit 3 = U, bit 1 = U & ~L, bit 0 = L;
+//   KIND 1 (the sign layer alone, k_used = 1): -0.5 W_0 (1001 or 0);
+//   KIND 2 (L = 1): -0.5 W_0, or for the binary code 1 - 2 W_0 (offset 1): +-0.5.
+template <int KIND>
+__device__ __forceinline__ uint32_t sign_nibbles(uint32_t x, bool binary) {
+    constexpr uint32_t kM1 = 0x11111111u, kM2 = 0x22222222u;
+    if (KIND == 0) {
+        const uint32_t u = x & kM2, l = x & kM1;
+        return (u << 2) | (u & ~(l << 1)) | l;
+    }
+    return (x << 3) | (KIND == 2 && binary ? kM1 : x);
+}
+
 // One pass of one row.  Paired storage: the pass's 32 blocks are 64 words in
 // two 16 KiB stages (t0: blocks 0..15, t1: 16..31); canonical: 32 words in one
 // stage.  A stage's 8 chunks of the row are read from the swizzled tile (128B
@@ -144,7 +160,7 @@ __device__ __forceinline__ void build_a(const uint4 (&q)[4], uint32_t xm, uint32
 // producer before its A registers are built and stored to TMEM (32 columns
 // per 4 chunks).
 template <int KIND>
-__device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
+__device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, int sgn,
                                              int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
     constexpr bool kPair = KIND <= 1;
 #pragma unroll
@@ -159,10 +175,14 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
             uint32_t v[32];
             if (kPair) {
                 const uint4 qq[4] = {q[4 * h], q[4 * h + 1], q[4 * h + 2], q[4 * h + 3]};
-                build_a<KIND>(qq, xm, v);
+                build_a<KIND>(qq, 0u, v);
             } else {
                 const uint4 qq[4] = {q[2 * h], q[2 * h + 1], q[2 * h], q[2 * h + 1]};
-                build_a<KIND>(qq, xm, v);
+                build_a<KIND>(qq, 0u, v);
+            }
+            if (sgn) {                          // warp-uniform: pass 0 only
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = sign_nibbles<KIND>(v[i], sgn == 2);
             }
             const int b4 = kPair ? 2 * t + h : h;
             if (dbg != 1 && dbg != 3)
@@ -188,9 +208,10 @@ __device__ __forceinline__ void pass_region_g(int Gp, int passes, int k_used, in
     s = pass_lo(k_used, last) - pass_lo(k_used, ps);
     first = (ps == region * Gp);
 }
-// |S_i|: 2^(L-1-i); the binary layer (offset 1) has |S_0| = 2.
+// |S_i|: 2^(L-1-i), the unit of a pass whose least significant layer is i.  The
+// binary code 1 - 2 W_0 (offset 1) is carried whole by its +-0.5 nibbles: unit 1.
 __device__ __forceinline__ unsigned long long layer_mag(int L, int offset, int i) {
-    if (i == 0 && offset) return 2ull;
+    if (i == 0 && offset) return 1ull;
     return 1ull << (L - 1 - i);
 }
 
@@ -307,5 +328,39 @@ __device__ __forceinline__ bool plane_sums_dispatch(int a, uint32_t dreg, int nb
     return false;
 }
 
+
+// E8M0 block scale factors in TMEM columns [sf_col, sf_col + 64) (warps of one lane-quarter
+// set, warp & 3 = quarter): columns 0..3 = 1.0 (SFA), columns 4(1+s)..4(1+s)+3 = 2^s (SFB of
+// passes with in-group weight 2^s); every byte of a column holds the same value.
+__device__ __forceinline__ void store_scale_factors(uint32_t tmem, int warp, int sf_col) {
+#pragma unroll
+    for (int blk = 0; blk < 4; ++blk) {
+        uint32_t v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            const int col = blk * 16 + c, sidx = col / 4;   // sidx 0 = SFA, 1 + s = 2^s
+            v[c] = 0x01010101u * (uint32_t)(127 + (sidx == 0 ? 0 : sidx - 1));
+        }
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+                tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(sf_col + blk * 16)),
+            "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+            "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+            : "memory");
+    }
+}
+// kind::mxf4 instruction descriptor: A, B = E2M1, scale format UE8M0, K = 64, M = 128, N = npad.
+__host__ __device__ constexpr uint32_t mxf4_idesc(int npad) {
+    return (1u << 7) | (1u << 10) | ((uint32_t)(npad >> 3) << 17) | (1u << 23) | ((uint32_t)(kTcRows >> 4) << 24);
+}
+// Exact f32 accumulation bound: passes per accumulator group for K padded columns
+// (|D| < 3 K 2^G <= 2^24, pb_gemm_tc.cu make_plan), at most 7 (SFB exponents 0..13).
+inline int tc_group_passes(int64_t kwords) {
+    int k = 0;
+    while (((int64_t)1 << k) < 3 * kwords * 32) ++k;
+    int G = 24 - k;
+    if (G > 15) G = 15;
+    return G / 2;
+}
 
 }  // namespace pb

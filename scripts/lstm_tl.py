@@ -1,0 +1,30 @@
+"""Per-step timeline of the persistent LSTM kernel (PB_TC_DEBUG=6): medians over CTAs of
+step start -> h_full -> B built -> MMAs done -> arrived (us, relative to each step's start)."""
+import math, os, sys
+import numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2003_00822_b200 as pb
+H, T, L, B = 2048, 8, int(os.environ.get("L", 4)), int(os.environ.get("B", 1))
+rng = np.random.default_rng(1)
+W = lambda: torch.from_numpy(pb.interleave_gates((rng.standard_normal((4 * H, H)) / math.sqrt(H)).astype(np.float32))).cuda()
+wi, wh = pb.PackedWeights.quantize_device(W(), L), pb.PackedWeights.quantize_device(W(), L)
+xs = torch.randn(T, B, H, device="cuda")
+h0, c0 = torch.tanh(torch.randn(B, H, device="cuda")), torch.randn(B, H, device="cuda")
+bi = torch.zeros(4 * H, device="cuda")
+ws = pb.Workspace(pb.pb_lstm_seq_workspace_bytes(T, B, H, H, 16))
+pb.lstm_seq(xs, h0, c0, wi, wh, bi, ws=ws)
+torch.cuda.synchronize()
+pb.debug_timeline()
+pb.lstm_seq(xs, h0, c0, wi, wh, bi, ws=ws)
+torch.cuda.synchronize()
+rec = pb.debug_timeline()
+r = rec[rec[:, 0] == 7]
+print("records", len(r))
+for t in range(T):
+    s = r[r[:, 2] == t]
+    t0 = s[:, 3].min()
+    f = lambda c: np.median((s[:, c] - t0) / 1e3)
+    mx = lambda c: ((s[:, c] - t0) / 1e3).max()
+    print(f"step {t}: start->h_full {f(4):6.2f} (max {mx(4):6.2f})  B built {f(5):6.2f}  MMAs done {f(6):6.2f} (max {mx(6):6.2f})  arrived {f(8):6.2f} (max {mx(8):6.2f})  finishers {int(s[:,7].sum())}")
+print("cycles (median over CTAs, steps >= 1): h_full->casts done", np.median(r[r[:,2]>0][:,7]),
+      " ballots", np.median(r[r[:,2]>0][:,9] // 1000000), " digit writes", np.median(r[r[:,2]>0][:,9] % 1000000))
