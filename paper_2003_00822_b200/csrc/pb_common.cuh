@@ -135,6 +135,39 @@ __device__ __forceinline__ bool digit_of_lane(uint32_t mine, int lane, int a, ui
     return !(lane & 1) && lane < a;
 }
 
+// The same digit rows without a ballot transpose, for an even a <= 16 (warp-collective):
+// every lane holds x_q of its column 32w + lane as the a-bit pattern u.  A lane first forms
+// its 8 digit nibbles (digit k in nibble 7 - k; digits >= ceil(a/2) are 0): the pairs of the
+// top-aligned pattern spread to 4-bit slots, then the e2m1 code of 2 d (as digit_regs, the
+// sign digit 0 in nibble 7).  The 8 lanes sharing r = lane & 3 then transpose their 8 x 8
+// nibble matrix in 3 butterfly stages (shfl_xor 16, 8, 4), after which lane 4e + r holds
+// register r of digit k = 7 - e: nibble j = the digit of column 4j + r.  Returns that
+// register; *k receives the digit (the caller stores it when k < ceil(a/2)).
+__device__ __forceinline__ uint32_t digit_regs_shfl(uint32_t u, int a, int lane, int& k) {
+    const uint32_t p = (u << (32 - a)) >> 16;        // pair j (bits 2j, 2j+1) = digit 7 - j
+    uint32_t x = (p | (p << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;                // pair j in nibble j: bit 0 = lo, bit 1 = hi
+    const uint32_t L = x & 0x11111111u, H = (x >> 1) & 0x11111111u;
+    const uint32_t gen = ((H | L) << 2) | (H << 1) | (H & L);             // 0, 2, 4, 6
+    const uint32_t sgn = (H << 3) | ((H | L) << 2) | ((H & ~L) << 1);     // 0, 2, -4, -2
+    x = (gen & 0x0FFFFFFFu) | (sgn & 0xF0000000u);
+    const int e = lane >> 2;
+    uint32_t t = __shfl_xor_sync(0xffffffffu, x, 16);
+    x = (e & 4) ? ((x & 0xFFFF0000u) | (t >> 16)) : ((x & 0x0000FFFFu) | (t << 16));
+    t = __shfl_xor_sync(0xffffffffu, x, 8);
+    x = (e & 2) ? ((x & 0xFF00FF00u) | ((t >> 8) & 0x00FF00FFu)) : ((x & 0x00FF00FFu) | ((t & 0x00FF00FFu) << 8));
+    t = __shfl_xor_sync(0xffffffffu, x, 4);
+    x = (e & 1) ? ((x & 0xF0F0F0F0u) | ((t >> 4) & 0x0F0F0F0Fu)) : ((x & 0x0F0F0F0Fu) | ((t & 0x0F0F0F0Fu) << 4));
+    k = 7 - e;
+    return x;
+}
+// Byte offset of register r of digit row n, word w in a tile set of N_pad rows (the layout of
+// put_b_operand).
+__device__ __forceinline__ uint32_t b_operand_offset(int npad, int64_t w, int n, int r) {
+    return (uint32_t)((w >> 1) * npad * 32 + (w & 1) * 128 + (n >> 3) * 256 + (n & 7) * 16 + r * 4);
+}
+
 // Next diagnostics-timeline record (pb_internal.h, pb_debug_timeline) or null when full.
 __device__ __forceinline__ long long* tl_record(long long* tl) {
     const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(tl), 1ull);

@@ -415,7 +415,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
 {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzled TMA tiles
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned as an offset into smem_raw (not through an integer cast), so the compiler
+    // keeps the shared window: every access through `bars` is LDS/STS, not a generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     Bars& bars = *reinterpret_cast<Bars*>(smem);
     constexpr uint32_t kBTile = NPAD * 32;                    // one MMA's B (64 columns)
     constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;  // one K-chunk (16 MMAs)

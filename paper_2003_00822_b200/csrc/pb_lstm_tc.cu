@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <mutex>
 
 #include "pb_common.cuh"
@@ -88,6 +89,7 @@ struct LPlan {
     int tiles, chunks;
     int slots, sf_col, d_col, wstages;
     int passes, Gp, regions;
+    int resident;              // the unit's A (all passes) stays in TMEM for every timestep
 };
 
 template <int NPAD>
@@ -96,7 +98,9 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     const __grid_constant__ CUtensorMap smap)
 {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte aligned as an offset into smem_raw (not through an integer cast), so the compiler
+    // keeps the shared window: every access through `bars` is LDS/STS, not a generic LD/ST
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     LBars& bars = *reinterpret_cast<LBars*>(smem);
     constexpr uint32_t kBTile = NPAD * 32;
     constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;
@@ -155,7 +159,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
         // ---------------------------------------------- weight tiles of this CTA's unit, every
         // timestep (L2-resident after the first), as far ahead as the ring allows
         int tc = 0;
-        for (int t = 0; t < T; ++t)
+        for (int t = 0; t < (p.resident ? 1 : T); ++t)
             for (int ps = 0; ps < p.passes; ++ps) {
                 const bool stored_pair = 2 * ps + 1 < g.L;
                 for (int h = 0; h < (stored_pair ? 2 : 1); ++h, ++tc) {
@@ -189,7 +193,8 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 pass_region_g(p.Gp, p.passes, g.k_used, ps, region, sexp, first);
                 const uint32_t dcol = tmem + (uint32_t)(p.d_col + region * NPAD);
                 const uint32_t sfb = tmem + (uint32_t)(p.sf_col + 4 * (1 + sexp));
-                mbar_wait(&bars.a_full[slot], phase);
+                if (p.resident) slot = (uint32_t)ps;
+                if (!p.resident || t == 0) mbar_wait(&bars.a_full[slot], phase);
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t a0 = tmem + slot * 128;
@@ -197,7 +202,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     for (int uu = 0; uu < 16; ++uu)
                         tc_mma(dcol, a0 + 8 * uu, bdesc0 + uu * (kBTile / 16), idesc, (uu == 0 && first) ? 0u : 1u,
                                sfa, sfb);
-                    tc_commit(&bars.a_empty[slot]);
+                    if (!p.resident) tc_commit(&bars.a_empty[slot]);
                 }
                 __syncwarp();
                 if (++slot == (uint32_t)p.slots) {
@@ -230,7 +235,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 pend_slot = -1;
             }
         };
-        for (int t = 0; t < T; ++t)
+        for (int t = 0; t < (p.resident ? 1 : T); ++t)
             for (int ps = 0; ps < p.passes; ++ps, ++pc) {
                 const bool stored_pair = 2 * ps + 1 < g.L;
                 const bool use_lo = 2 * ps + 1 < g.k_used;
@@ -243,7 +248,8 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 mbar_wait(&bars.w_full[st0], (uint32_t)((tc / p.wstages) & 1));
                 if (stored_pair) mbar_wait(&bars.w_full[st1], (uint32_t)(((tc + 1) / p.wstages) & 1));
                 publish();
-                mbar_wait(&bars.a_empty[slot], (uint32_t)(sphase ^ 1));
+                if (p.resident) slot = ps;                    // slots fresh: nothing to wait for
+                else mbar_wait(&bars.a_empty[slot], (uint32_t)(sphase ^ 1));
                 tc_fence_after();
                 const int kind = stored_pair ? (use_lo ? 0 : 1) : 2;
                 const int sgn = ps == 0 ? (g.offset ? 2 : 1) : 0;   // the sign layer's pass: signed nibbles
@@ -358,56 +364,97 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             if (t == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
             mbar_wait(&bars.h_full, (uint32_t)(t & 1));
             if (g.tl) tm[1] = gtimer();
+            long long ck[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            if (g.tl) ck[0] = clock64();
             const int par = t & 1;
             // ---- a1-a2: the digits of this CTA's chunk into the B operand: items (b, word), each
             //      warp 8 items at a time (independent ballot chains), values from the SMEM copy
-            const int nit = B * kChunkWords;
             // the exact fp32 cast of act_cast (pb_common.cuh) when every f_b of the step is in range
             bool fast = a <= 24;
             for (int b = 0; b < B && fast; ++b) fast = bars.scl[par][b] != 0.f;
             const float lim = (float)(1 << ((a <= 24 ? a : 24) - 1));
-            for (int k0 = 0; ew + kEpiWarps * k0 < nit; k0 += 8) {
-                uint32_t u[8], mm[8];
+            const bool shfl_digits = !(a & 1) && a <= 16;
+            const uint32_t amask = a >= 32 ? ~0u : ((1u << a) - 1u);
+#ifdef PB_LSTM_TWICE
+            for (int rep = 0; rep < 2; ++rep) {
+            if (rep == 1 && g.tl) ck[0] = clock64();
+#endif
+            // one round = the 32 words of batch column b (warp ew takes words ew, ew + 4, ...):
+            // 8 independent loads, casts and transposes per warp, no branches inside the round
+            static_assert(kEpiWarps * 8 == kChunkWords, "a round covers one batch column");
+            const int cvalid = H - kc * kChunkWords * 32;        // valid columns of this K-chunk
+#pragma unroll 1
+            for (int b = 0; b < B; ++b) {
+                uint32_t u[8];
+                float v[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const int it = ew + kEpiWarps * (k0 + k);
-                    const int b = it / kChunkWords, cl = (it - b * kChunkWords) * 32 + lane;
-                    float v = 0.f;
-                    if (it < nit && (int64_t)kc * kChunkWords * 32 + cl < H)
-                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(hbuf_s + (uint32_t)((b * kChunkWords * 32 + cl) * 4)));
-                    if (fast) {
-                        float tq = v * bars.scl[par][b];
-                        tq = fminf(fmaxf(tq, -lim), lim - 1.0f);
-                        u[k] = (uint32_t)__float2int_rz(tq);
-                    } else {
-                        u[k] = it < nit ? (uint32_t)act_cast(v, bars.f[par][b], a) : 0u;
-                    }
-                    mm[k] = 0;
+                    const int cl = (ew + kEpiWarps * k) * 32 + lane;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[k]) : "r"(hbuf_s + (uint32_t)((b * kChunkWords * 32 + cl) * 4)));
+                    v[k] = cl < cvalid ? v[k] : 0.f;          // stale SMEM past the copied columns
                 }
+                if (fast) {
+                    const float sc = bars.scl[par][b];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        u[k] = (uint32_t)__float2int_rz(fminf(fmaxf(v[k] * sc, -lim), lim - 1.0f));
+                } else {
+                    const int f = bars.f[par][b];
 #pragma unroll 1
-                for (int j = 0; j < a; ++j) {
+                    for (int k = 0; k < 8; ++k) u[k] = (uint32_t)act_cast(v[k], f, a);
+                }
+                if (g.tl && b == 0) {
+                    uint32_t z = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) z |= u[k];
+                    asm volatile("" ::"r"(z));
+                    ck[8] = clock64();
+                }
+                if (shfl_digits) {
+                    // even a <= 16: per-lane digit nibbles + a nibble transpose (no ballots)
+                    uint32_t reg[8];
+                    int dk = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) reg[k] = digit_regs_shfl(u[k] & amask, a, lane, dk);
+                    if (dk < nd) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            asm volatile("st.shared.u32 [%0], %1;" ::"r"(bstage_s + b_operand_offset(NPAD, ew + kEpiWarps * k, b * nd + dk, lane & 3)),
+                                         "r"(reg[k]) : "memory");
+                    }
+                } else {
+                    uint32_t mm[8];
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mm[k] = 0;
+#pragma unroll 1
+                    for (int j = 0; j < a; ++j) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const uint32_t w = __ballot_sync(0xffffffffu, (u[k] >> (a - 1 - j)) & 1u);
+                            if (lane == j) mm[k] = w;
+                        }
+                    }
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
-                        const uint32_t w = __ballot_sync(0xffffffffu, (u[k] >> (a - 1 - j)) & 1u);
-                        if (lane == j) mm[k] = w;
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int it = ew + kEpiWarps * (k0 + k);
-                    if (it < nit) {                               // warp-uniform
-                        const int b = it / kChunkWords, wl = it - b * kChunkWords;
                         uint4 dv;
                         if (digit_of_lane(mm[k], lane, a, dv))
-                            put_b_operand_smem(bstage_s, NPAD, wl, b * nd + (lane >> 1), dv);
-                        if (b == B - 1)
-                            for (int n = B * nd + lane; n < NPAD; n += 32)
-                                put_b_operand_smem(bstage_s, NPAD, wl, n, make_uint4(0, 0, 0, 0));
+                            put_b_operand_smem(bstage_s, NPAD, ew + kEpiWarps * k, b * nd + (lane >> 1), dv);
                     }
                 }
             }
+            if (B * nd < NPAD) {                               // zero digit rows past the batch
+#pragma unroll 1
+                for (int k = 0; k < 8; ++k)
+                    for (int n = B * nd + lane; n < NPAD; n += 32)
+                        put_b_operand_smem(bstage_s, NPAD, ew + kEpiWarps * k, n, make_uint4(0, 0, 0, 0));
+            }
+#ifdef PB_LSTM_TWICE
+            }
+#endif
+            if (g.tl) ck[1] = clock64();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA
             asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (g.tl) ck[2] = clock64();
             if (pt == 0) {
                 mbar_arrive(&bars.b_full);
                 mbar_arrive(&bars.h_empty);
@@ -417,6 +464,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             mbar_wait(&bars.d_full, (uint32_t)(t & 1));
             tc_fence_after();
             if (g.tl) tm[3] = gtimer();
+            if (g.tl) ck[3] = clock64();
             unsigned long long tot1 = 0;
             for (int r = 0; r < p.regions; ++r) {
                 int last = (r + 1) * p.Gp - 1;
@@ -461,6 +509,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bars.d_empty);
+            if (g.tl) ck[4] = clock64();
             auto tot_of = [&](int b) -> unsigned long long {
                 return (!kWide && B == 1) ? tot1 : ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u);
             };
@@ -475,11 +524,13 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             } else if (p.chunks > 1) {
                 mbar_wait_cluster(&bars.red_full, (uint32_t)(t & 1));
             }
+            if (g.tl) ck[5] = clock64();
             if (finish) {
                 const float* c_in = t == 0 ? g.c0 : (g.c_seq ? g.c_seq + (int64_t)(t - 1) * B * H : (((t - 1) & 1) ? g.cbuf1 : g.cbuf0));
                 float* c_out = g.c_seq ? g.c_seq + (int64_t)t * B * H : (t == T - 1 ? g.c_last : ((t & 1) ? g.cbuf1 : g.cbuf0));
                 float* h_out = g.h_seq + (int64_t)t * B * H;
                 mbar_wait(&bars.gx_full[t & 1], (uint32_t)((t >> 1) & 1));
+                if (g.tl) ck[6] = clock64();
                 for (int b = 0; b < B; ++b) {
                     unsigned long long tt = tot_of(b);
                     for (int r = 1; r < p.chunks; ++r)
@@ -508,12 +559,19 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             }
             // ---- publish h_{t+1}: every CTA arrives (the 128 threads' stores are ordered before
             //      thread 0's release by bar.sync)
+            if (g.tl) ck[7] = clock64();
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (pt == 0) grid_arrive(g.gbar);
             if (g.tl && pt == 0) {
                 long long* rr = tl_record(g.tl);
                 if (rr) {
                     const long long rec[10] = {7, blockIdx.x, t, tm[0], tm[1], tm[2], tm[3], finish ? 1 : 0, gtimer(), 0};
+                    for (int k = 0; k < 10; ++k) rr[k] = rec[k];
+                }
+                rr = tl_record(g.tl);
+                if (rr) {
+                    const long long rec[10] = {8, blockIdx.x, t, ck[1] - ck[0], ck[2] - ck[0], ck[3] - ck[0], ck[4] - ck[0],
+                                               ck[5] - ck[0], ck[8] - ck[0], ck[7] - ck[0]};
                     for (int k = 0; k < 10; ++k) rr[k] = rec[k];
                 }
             }
@@ -529,6 +587,12 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
 uint32_t lstm_fixed_smem(int B, int npad, int chunks) {
     return 1024 + kHdrBytes + (uint32_t)(kChunkWords / 2) * npad * 32 + (uint32_t)B * kTcRows * 8 +
            (uint32_t)B * kChunkWords * 32 * 4 + (uint32_t)(chunks - 1) * B * kTcRows * 8 + 2u * B * kTcRows * 4;
+}
+
+// Comparison knob: NAME=0 disables a default-on mode.
+bool getenv_flag_off(const char* name) {
+    const char* ev = getenv(name);
+    return ev && ev[0] == '0';
 }
 
 bool make_lplan(const LstmArgs& g, int npad, int sms, LPlan& p)
@@ -548,6 +612,9 @@ bool make_lplan(const LstmArgs& g, int npad, int sms, LPlan& p)
     p.slots = p.sf_col / 128;
     if (p.slots > kMaxSlots) p.slots = kMaxSlots;
     if (p.slots < 2) return false;
+    // A of every pass resident (converted once, at step 0) when it fits the A ring
+    p.resident = (p.passes <= p.slots && !getenv_flag_off("PB_LSTM_RESIDENT")) ? 1 : 0;
+    if (p.resident) p.slots = p.passes;
     p.wstages = (int)((kSmemMax - lstm_fixed_smem(g.B, npad, p.chunks)) / kWTileBytes);
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     // >= 4: the two converter h-sets wait on the tiles of consecutive passes (2 tiles each); with

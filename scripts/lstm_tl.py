@@ -28,3 +28,10 @@ for t in range(T):
     print(f"step {t}: start->h_full {f(4):6.2f} (max {mx(4):6.2f})  B built {f(5):6.2f}  MMAs done {f(6):6.2f} (max {mx(6):6.2f})  arrived {f(8):6.2f} (max {mx(8):6.2f})  finishers {int(s[:,7].sum())}")
 print("cycles (median over CTAs, steps >= 1): h_full->casts done", np.median(r[r[:,2]>0][:,7]),
       " ballots", np.median(r[r[:,2]>0][:,9] // 1000000), " digit writes", np.median(r[r[:,2]>0][:,9] % 1000000))
+c = rec[rec[:, 0] == 8]
+c = c[c[:, 2] > 0]
+if len(c):
+    names = ["digits", "B built", "d_full", "drained", "reduced", "casts", "pre-arrive"]
+    for fin in (0, 1):
+        s = c[np.isin(c[:, 1], r[(r[:, 7] == fin)][:, 1])]
+        print(("leader " if fin else "other  ") + "  ".join(f"{n} {np.median(s[:, 3 + i]) / 1.965e3:5.2f}" for i, n in enumerate(names)) + " us after h_full (clock64)")
