@@ -865,7 +865,8 @@ size_t pb_lstm_seq_workspace_bytes(int64_t steps, int64_t batch, int64_t in_cols
     return pb::align_up(pb_workspace_bytes(cols, k, act_bits)) +
            pb::align_up(sizeof(float) * (size_t)cols * 4 * (size_t)hidden) +
            2 * pb::align_up(sizeof(float) * (size_t)batch * (size_t)hidden) +
-           pb::align_up(sizeof(unsigned long long) * 2 * pb::kLstmMaxB);   // persistent kernel: max|h| slots
+           pb::align_up(sizeof(unsigned long long) * 2 * pb::kLstmMaxB) +   // persistent kernel: max|h| slots
+           pb::lstm_xchg_bytes(hidden);                                     // B = 1 tagged h exchange
 }
 
 pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float* h0, const float* c0,
@@ -933,6 +934,11 @@ pb_status pb_lstm_seq(const float* x, int64_t steps, int64_t batch, const float*
         la.tl = pb::debug_tl();
         la.maxslot = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(cb[1]) +
                                                            pb::align_up(sizeof(float) * (size_t)batch * (size_t)H));
+        // [stepctr][pad to 256][mxs 2 x kLstmMaxTiles][hx 2 x H]
+        char* xg = reinterpret_cast<char*>(la.maxslot) + pb::align_up(sizeof(unsigned long long) * 2 * pb::kLstmMaxB);
+        la.stepctr = reinterpret_cast<unsigned long long*>(xg);
+        la.mxs = reinterpret_cast<unsigned long long*>(xg + 256);
+        la.hx = la.mxs + 2 * pb::kLstmMaxCtas * pb::kLstmMaxTiles;
         const bool room = (lw.npad || lw.wbs) &&
                           (size_t)((la.R + pb::kTcRows - 1) / pb::kTcRows) * (size_t)batch * pb::kTcRows * 8 <=
                               lw.off_f - lw.off_slots;

@@ -162,6 +162,8 @@ struct GemmArgs {
 // Persistent LSTM recurrence (pb_lstm_tc.cu): all T timesteps of
 // h_{t+1}, c_{t+1} = cell(gx[t] + W_hh h_t, c_t) in one launch, one CTA per (row tile,
 // K-chunk) unit of W_hh, a grid barrier per timestep.
+constexpr int kLstmMaxTiles = 64;   // persistent LSTM: 128-row tiles of W_hh (H <= 2048)
+constexpr int kLstmMaxCtas = 160;   // persistent LSTM grid (tiles x chunks <= #SMs)
 constexpr int kLstmMaxB = 32;        // batch columns (digit columns B * ceil(a/2) <= 128)
 struct LstmArgs {
     const uint32_t* bits;   // W_hh [L][4H][kwords], gate-interleaved rows (row 4k + gate)
@@ -181,9 +183,18 @@ struct LstmArgs {
     int* counters;                // [tiles], zero between calls
     int* gbar;                    // monotonic grid-barrier counter (+2^20 per timestep)
     unsigned long long* maxslot;  // [2][kLstmMaxB] epoch-tagged max|h| (zero-filled once, never reset)
+    // B = 1 exchange without a grid barrier: h_t and the per-tile max|h_t| as self-validating
+    // 64-bit values (tag << 32) | float bits, tag = (uint32)(step counter at call start + t)
+    unsigned long long* hx;       // [2][H] tagged h_t (by t & 1)
+    unsigned long long* mxs;      // [2][CTAs][kLstmMaxTiles] mailboxes: tagged per-tile max|h_t|
+    unsigned long long* stepctr;  // + T per call (workspace-resident, zero-filled once)
     long long* tl;                // diagnostics timeline (PB_TC_DEBUG=6) or null
 };
 int lstm_persist_npad(int64_t batch, int32_t a);
+// Workspace of the B = 1 tagged exchange: step counter, per-tile slots, h_t by parity.
+inline size_t lstm_xchg_bytes(int64_t H) {
+    return align_up(256 + sizeof(unsigned long long) * (2 * (size_t)kLstmMaxCtas * kLstmMaxTiles + 2 * (size_t)H));
+}
 bool lstm_persist_supported(const LstmArgs& g);
 cudaError_t launch_lstm_persist(const LstmArgs& g, cudaStream_t s);
 

@@ -56,6 +56,7 @@ struct LBars {
     uint32_t tmem_base;
     int fin;                                   // this step: the CTA completed its tile (1) or not
     float red[kEpiWarps][kLstmMaxB];           // per-warp partial max|h[b,:]|
+    float pmax[2][kEpiWarps];                  // B = 1 producer: per-warp max|h_{t+1}| (by t & 1)
     int f[2][kLstmMaxB];                       // f_b of step t at [t & 1]
     double sc[2][kLstmMaxB];                   // s_w 2^-f_b
     float scl[2][kLstmMaxB];                   // 2^f_b as fp32 (the cast's fast path)
@@ -112,6 +113,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
     const uint32_t redbuf_s = smem_u32(hbuf + (size_t)g.B * kChunkWords * 32 * 4);   // [chunks-1][b][128] u64
     float* gxbuf = reinterpret_cast<float*>(hbuf + (size_t)g.B * kChunkWords * 32 * 4 +
                                             (size_t)(p.chunks - 1) * g.B * kTcRows * 8);   // [2][b][128] fp32
+    float* cst = gxbuf + 2 * g.B * kTcRows;                     // [b][32] the leader's cell state
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rt = blockIdx.x / p.chunks, kc = blockIdx.x - rt * p.chunks;
     const int T = g.T;
@@ -272,9 +274,11 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             }
         publish();
     } else if (warp == 2) {
-        // ---------------------------------------------- step gate: once h_t is complete on every
-        // CTA (grid barrier of step t-1), copy this CTA's K-chunk of h_t (B rows of <= 1024
-        // floats) into SMEM for the prologue (1-D bulk copies completing on h_full)
+        // ---------------------------------------------- step gate: the tile's gx[t] rows (leader),
+        // and for B > 1: once h_t is complete on every CTA (grid barrier of step t-1), this CTA's
+        // K-chunk of h_t (B rows of <= 1024 floats) into SMEM (1-D bulk copies on h_full) and
+        // f_b from the epoch-tagged atomicMax slots.  (B = 1 exchanges h through tagged values,
+        // read by the epilogue warps themselves.)
         pdl_wait();
         unsigned long long gbase = 0;
         if (lane == 0) gbase = grid_base(g.gbar);
@@ -283,8 +287,9 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
         const int ncol = H - c0 < kChunkWords * 32 ? H - c0 : kChunkWords * 32;
         const int64_t r0 = (int64_t)rt * kTcRows;
         const int nrow = g.R - r0 < kTcRows ? (int)(g.R - r0) : kTcRows;
+        const bool tagx = g.B == 1;
         for (int t = 0; t < T; ++t) {
-            if (t > 0) mbar_wait(&bars.h_empty, (uint32_t)((t - 1) & 1));   // the prologue read h_{t-1}
+            if (t > 0) mbar_wait(&bars.h_empty, (uint32_t)((t - 1) & 1));   // the prologue of step t-1 is done
             if (lane == 0 && kc == 0) {
                 // the tile's rows of gx[t] (no dependence on h): in flight while the step waits
                 mbar_arrive_expect_tx(&bars.gx_full[t & 1], (uint32_t)(g.B * nrow * 4));
@@ -292,6 +297,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     bulk_g2s(gxbuf + ((t & 1) * g.B + b) * kTcRows, g.gx + ((int64_t)t * g.B + b) * g.R + r0,
                              (uint32_t)(nrow * 4), &bars.gx_full[t & 1]);
             }
+            if (tagx) continue;
             if (lane == 0) {
                 if (t > 0) {
                     const unsigned long long* c = reinterpret_cast<const unsigned long long*>(g.gbar);
@@ -306,8 +312,6 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                              &bars.h_full);
             }
             __syncwarp();
-            // f_b of step t > 0 from the maxima the producers of h_t published (epoch-tagged
-            // atomicMax slots, pb_internal.h), while the copies fly (step 0: the prologue reads h0)
             if (t > 0 && lane < g.B) {
                 const unsigned long long v = __ldcg(g.maxslot + ((t & 1) * kLstmMaxB + lane));
                 const int f = act_frac_of(__uint_as_float((uint32_t)v), g.a);
@@ -330,12 +334,34 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
         const int64_t row = (int64_t)rt * kTcRows + m;
         const uint32_t bstage_s = smem_u32(bstage);
         const uint32_t hbuf_s = smem_u32(hbuf);
-        pdl_wait();                                  // h0 / gx come from earlier kernels
+        const bool tagx = B == 1;                     // h exchanged as tagged values (below)
+        const int cbase = kc * kChunkWords * 32;      // first column of this CTA's K-chunk
+        const int cvalid = H - cbase;                 // valid columns of the chunk (may exceed 1024)
+        const bool finish = kc == 0;                  // the tile's leader finishes it (the cell)
+        pdl_wait();                                   // h0 / c0 / gx come from earlier kernels
         if (pt == 0) bars.epoch0 = grid_base(g.gbar) / kGridStride;
+        // tag base of this call: h_t (t >= 1) carries (uint32)(sbase + t); CTA 0 advances the
+        // counter by T at its end (after every CTA read it: step 1 needs every tile's step 0)
+        const unsigned long long sbase = ld_acquire_gpu_u64(g.stepctr);
+        // diagnostics: 3 records per step at indices reserved once (no atomic inside the steps)
+        long long* tlb = nullptr;
+        if (g.tl && pt == 0) {
+            const unsigned long long i0 = atomicAdd(reinterpret_cast<unsigned long long*>(g.tl), 3ull * T);
+            if (i0 + 3ull * T <= (unsigned long long)kTlRecords) tlb = g.tl + 10 + 10 * (long long)i0;
+        }
+        // the cell state of the leader's 32 hidden units stays in SMEM across timesteps
+        if (finish && (lane & 3) == 0 && row < R)
+            for (int b = 0; b < B; ++b) cst[b * 32 + (m >> 2)] = g.c0[(int64_t)b * H + (row >> 2)];
         for (int t = 0; t < T; ++t) {
-            // ---- a1: f_b from max|h_t[b,:]| (reading G8).  Step 0 reads all of h0; h_t for t > 0
-            //      comes with its maxima, published by the CTAs that produced it (epoch-tagged
-            //      atomicMax slots: (barrier instance << 32) | float bits, never reset)
+            const int par = t & 1;
+            long long tm[6] = {0, 0, 0, 0, 0, 0};
+            long long ck[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            if (g.tl) tm[0] = gtimer();
+            // ---- a1: f_b from max|h_t[b,:]| (reading G8).  Step 0 reads all of h0.  For t > 0 the
+            //      CTAs that produced h_t published its maxima: B = 1 per-tile tagged slots, read
+            //      together with the chunk's tagged h values (one L2 round trip, no barrier);
+            //      B > 1 epoch-tagged atomicMax slots behind the grid barrier (warp 2)
+            float hv0[8];                              // B = 1: this thread's 8 values of h_t
             if (t == 0) {
                 for (int b = 0; b < B; ++b) {
                     const float4* x4 = reinterpret_cast<const float4*>(g.h0 + (int64_t)b * H);
@@ -348,6 +374,13 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
                     if (lane == 0) bars.red[ew][b] = mx;
                 }
+                if (tagx) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int cl = (ew + kEpiWarps * k) * 32 + lane;
+                        hv0[k] = cl < cvalid ? __ldcg(g.h0 + cbase + cl) : 0.f;
+                    }
+                }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
                 if (pt < B) {
                     float mx = bars.red[0][pt];
@@ -358,40 +391,85 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     const int f = bars.f[0][pt];
                     bars.scl[0][pt] = (f >= -126 && f <= 127) ? __int_as_float((127 + f) << 23) : 0.f;
                 }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+            } else if (tagx) {
+                const uint32_t tag = (uint32_t)(sbase + (unsigned long long)t);
+                const unsigned long long* hx = g.hx + (int64_t)par * H + cbase;
+                // this CTA's mailbox: one tagged max|h_t| per tile, written by the tiles' leaders
+                const unsigned long long* sl = g.mxs + ((int64_t)par * gridDim.x + blockIdx.x) * kLstmMaxTiles;
+                // warp 0 polls the tiles' slots (2 per lane); then every thread loads its 8 values
+                // once (written before the slots; re-polled only if a tag is still old)
+                unsigned long long hv[8], sv = (unsigned long long)tag << 32;
+                int rounds = 0;
+                if (ew == 0) {
+                    unsigned long long s0, s1;
+                    bool ok;
+                    do {
+                        ++rounds;
+                        s0 = lane < p.tiles ? ld_relaxed_gpu_u64(sl + lane) : (unsigned long long)tag << 32;
+                        s1 = lane + 32 < p.tiles ? ld_relaxed_gpu_u64(sl + lane + 32) : (unsigned long long)tag << 32;
+                        ok = (uint32_t)(s0 >> 32) == tag && (uint32_t)(s1 >> 32) == tag;
+                    } while (!__all_sync(0xffffffffu, ok));
+                    sv = __uint_as_float((uint32_t)s0) > __uint_as_float((uint32_t)s1) ? s0 : s1;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int cl = (ew + kEpiWarps * k) * 32 + lane;
+                    hv[k] = cl < cvalid ? ld_relaxed_gpu_u64(hx + cl) : (unsigned long long)tag << 32;
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int cl = (ew + kEpiWarps * k) * 32 + lane;
+                    while ((uint32_t)(hv[k] >> 32) != tag) hv[k] = ld_relaxed_gpu_u64(hx + cl);
+                }
+                if (g.tl) {
+                    tm[4] = gtimer();
+                    tm[5] = rounds;
+                }
+                float mx = __uint_as_float((uint32_t)sv);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (lane == 0) bars.red[ew][0] = mx;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) hv0[k] = __uint_as_float((uint32_t)hv[k]);
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                mx = fmaxf(fmaxf(bars.red[0][0], bars.red[1][0]), fmaxf(bars.red[2][0], bars.red[3][0]));
+                const int f = act_frac_of(mx, a);
+                if (pt == 0) {
+                    bars.f[par][0] = f;
+                    bars.sc[par][0] = col_scale(g.scale, f);
+                    bars.scl[par][0] = (f >= -126 && f <= 127) ? __int_as_float((127 + f) << 23) : 0.f;
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
             }
-            long long tm[6] = {0, 0, 0, 0, 0, 0};
-            if (g.tl) tm[0] = gtimer();
-            if (t == 0) asm volatile("bar.sync 1, 128;" ::: "memory");
-            mbar_wait(&bars.h_full, (uint32_t)(t & 1));
+            if (!tagx) mbar_wait(&bars.h_full, (uint32_t)(t & 1));
             if (g.tl) tm[1] = gtimer();
-            long long ck[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
             if (g.tl) ck[0] = clock64();
-            const int par = t & 1;
-            // ---- a1-a2: the digits of this CTA's chunk into the B operand: items (b, word), each
-            //      warp 8 items at a time (independent ballot chains), values from the SMEM copy
+            // ---- a1-a2: the digits of this CTA's chunk into the B operand.  One round = the 32
+            //      words of batch column b (warp ew takes words ew, ew + 4, ...): 8 independent
+            //      casts and transposes per warp, no branches inside the round
             // the exact fp32 cast of act_cast (pb_common.cuh) when every f_b of the step is in range
             bool fast = a <= 24;
             for (int b = 0; b < B && fast; ++b) fast = bars.scl[par][b] != 0.f;
             const float lim = (float)(1 << ((a <= 24 ? a : 24) - 1));
             const bool shfl_digits = !(a & 1) && a <= 16;
             const uint32_t amask = a >= 32 ? ~0u : ((1u << a) - 1u);
-#ifdef PB_LSTM_TWICE
-            for (int rep = 0; rep < 2; ++rep) {
-            if (rep == 1 && g.tl) ck[0] = clock64();
-#endif
-            // one round = the 32 words of batch column b (warp ew takes words ew, ew + 4, ...):
-            // 8 independent loads, casts and transposes per warp, no branches inside the round
             static_assert(kEpiWarps * 8 == kChunkWords, "a round covers one batch column");
-            const int cvalid = H - kc * kChunkWords * 32;        // valid columns of this K-chunk
 #pragma unroll 1
             for (int b = 0; b < B; ++b) {
                 uint32_t u[8];
                 float v[8];
+                if (tagx) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    const int cl = (ew + kEpiWarps * k) * 32 + lane;
-                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[k]) : "r"(hbuf_s + (uint32_t)((b * kChunkWords * 32 + cl) * 4)));
-                    v[k] = cl < cvalid ? v[k] : 0.f;          // stale SMEM past the copied columns
+                    for (int k = 0; k < 8; ++k) v[k] = hv0[k];
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const int cl = (ew + kEpiWarps * k) * 32 + lane;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[k]) : "r"(hbuf_s + (uint32_t)((b * kChunkWords * 32 + cl) * 4)));
+                        v[k] = cl < cvalid ? v[k] : 0.f;      // stale SMEM past the copied columns
+                    }
                 }
                 if (fast) {
                     const float sc = bars.scl[par][b];
@@ -448,9 +526,6 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     for (int n = B * nd + lane; n < NPAD; n += 32)
                         put_b_operand_smem(bstage_s, NPAD, ew + kEpiWarps * k, n, make_uint4(0, 0, 0, 0));
             }
-#ifdef PB_LSTM_TWICE
-            }
-#endif
             if (g.tl) ck[1] = clock64();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA
             asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -515,7 +590,6 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             };
             // ---- a5: a tile's K-chunks are the CTAs of one cluster: the others put their exact
             //      partial sums into the leader's SMEM (DSMEM) and the leader finishes the tile
-            const bool finish = kc == 0;
             if (!finish) {
                 const uint32_t rb = mapa_shared(redbuf_s + (uint32_t)(((kc - 1) * B * kTcRows + m) * 8), 0);
                 for (int b = 0; b < B; ++b) st_cluster_u64(rb + (uint32_t)(b * kTcRows * 8), tot_of(b));
@@ -526,9 +600,9 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             }
             if (g.tl) ck[5] = clock64();
             if (finish) {
-                const float* c_in = t == 0 ? g.c0 : (g.c_seq ? g.c_seq + (int64_t)(t - 1) * B * H : (((t - 1) & 1) ? g.cbuf1 : g.cbuf0));
-                float* c_out = g.c_seq ? g.c_seq + (int64_t)t * B * H : (t == T - 1 ? g.c_last : ((t & 1) ? g.cbuf1 : g.cbuf0));
                 float* h_out = g.h_seq + (int64_t)t * B * H;
+                const uint32_t tag1 = (uint32_t)(sbase + (unsigned long long)t + 1);   // tag of h_{t+1}
+                unsigned long long* hx1 = g.hx + (int64_t)((t + 1) & 1) * H;
                 mbar_wait(&bars.gx_full[t & 1], (uint32_t)((t >> 1) & 1));
                 if (g.tl) ck[6] = clock64();
                 for (int b = 0; b < B; ++b) {
@@ -543,39 +617,54 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     if ((lane & 3) == 0 && row < R) {
                         const int64_t i = (int64_t)b * H + (row >> 2);
                         float cn;
-                        lstm_cell(gi, gf, gg, go, c_in[i], hn, cn);
+                        lstm_cell(gi, gf, gg, go, cst[b * 32 + (m >> 2)], hn, cn);
+                        cst[b * 32 + (m >> 2)] = cn;
+                        if (tagx && t + 1 < T)
+                            st_relaxed_gpu_u64(hx1 + (row >> 2), ((unsigned long long)tag1 << 32) | __float_as_uint(hn));
                         h_out[i] = hn;
-                        c_out[i] = cn;
-                        if (g.c_seq && t == T - 1) g.c_last[i] = cn;
+                        if (g.c_seq) g.c_seq[(int64_t)t * B * H + i] = cn;
+                        if (t == T - 1) g.c_last[i] = cn;
                     }
                     // max|h_{t+1}[b,:]| over this warp's 8 hidden units -> step t+1's f_b
                     float mh = fabsf(hn);
 #pragma unroll
                     for (int o = 16; o; o >>= 1) mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, o));
-                    if (lane == 0 && t + 1 < T)
-                        atomicMax(g.maxslot + (((t + 1) & 1) * kLstmMaxB + b),
-                                  ((bars.epoch0 + (unsigned long long)t + 1) << 32) | __float_as_uint(mh));
+                    if (lane == 0 && t + 1 < T) {
+                        if (tagx)
+                            bars.pmax[par][ew] = mh;
+                        else
+                            atomicMax(g.maxslot + (((t + 1) & 1) * kLstmMaxB + b),
+                                      ((bars.epoch0 + (unsigned long long)t + 1) << 32) | __float_as_uint(mh));
+                    }
                 }
             }
-            // ---- publish h_{t+1}: every CTA arrives (the 128 threads' stores are ordered before
+            // ---- publish h_{t+1}.  B = 1: the tile's max|h| slot after the 4 warps' maxima; B > 1:
+            //      every CTA arrives at the grid barrier (the 128 threads' stores are ordered before
             //      thread 0's release by bar.sync)
             if (g.tl) ck[7] = clock64();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (pt == 0) grid_arrive(g.gbar);
-            if (g.tl && pt == 0) {
-                long long* rr = tl_record(g.tl);
-                if (rr) {
-                    const long long rec[10] = {7, blockIdx.x, t, tm[0], tm[1], tm[2], tm[3], finish ? 1 : 0, gtimer(), 0};
-                    for (int k = 0; k < 10; ++k) rr[k] = rec[k];
-                }
-                rr = tl_record(g.tl);
-                if (rr) {
-                    const long long rec[10] = {8, blockIdx.x, t, ck[1] - ck[0], ck[2] - ck[0], ck[3] - ck[0], ck[4] - ck[0],
-                                               ck[5] - ck[0], ck[8] - ck[0], ck[7] - ck[0]};
-                    for (int k = 0; k < 10; ++k) rr[k] = rec[k];
-                }
+            if (!tagx || finish) asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (!tagx) {
+                if (pt == 0) grid_arrive(g.gbar);
+            } else if (finish && t + 1 < T) {
+                // every CTA's mailbox slot of this tile (distinct lines per reader: no polled hot spot)
+                const float mh = fmaxf(fmaxf(bars.pmax[par][0], bars.pmax[par][1]), fmaxf(bars.pmax[par][2], bars.pmax[par][3]));
+                const unsigned long long sv = ((unsigned long long)(uint32_t)(sbase + (unsigned long long)t + 1) << 32) | __float_as_uint(mh);
+                for (int i = pt; i < (int)gridDim.x; i += 128)
+                    st_relaxed_gpu_u64(g.mxs + ((int64_t)((t + 1) & 1) * gridDim.x + i) * kLstmMaxTiles + rt, sv);
+                if (g.tl && pt == 0) ck[6] = gtimer();
+            }
+            if (tlb) {
+                long long* rr = tlb + 30 * t;
+                const long long rec[30] = {7, blockIdx.x, t, tm[0], tm[1], tm[2], tm[3], finish ? 1 : 0, gtimer(), 0,
+                                           8, blockIdx.x, t, ck[1] - ck[0], ck[2] - ck[0], ck[3] - ck[0], ck[4] - ck[0],
+                                           ck[5] - ck[0], ck[8] - ck[0], ck[7] - ck[0],
+                                           9, blockIdx.x, t, tm[4], tm[5], finish ? ck[6] : 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int k = 0; k < 30; ++k) rr[k] = rec[k];
             }
         }
+        // the next call's tags start past this call's: CTA 0 advances the step counter
+        if (blockIdx.x == 0 && pt == 0) asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(g.stepctr), "l"((unsigned long long)T) : "memory");
     }
     tc_fence_before();
     cluster_sync();                                // no CTA leaves while its SMEM may be written
@@ -586,7 +675,8 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
 // leader's buffer for the other chunks' partial sums.
 uint32_t lstm_fixed_smem(int B, int npad, int chunks) {
     return 1024 + kHdrBytes + (uint32_t)(kChunkWords / 2) * npad * 32 + (uint32_t)B * kTcRows * 8 +
-           (uint32_t)B * kChunkWords * 32 * 4 + (uint32_t)(chunks - 1) * B * kTcRows * 8 + 2u * B * kTcRows * 4;
+           (uint32_t)B * kChunkWords * 32 * 4 + (uint32_t)(chunks - 1) * B * kTcRows * 8 + 2u * B * kTcRows * 4 +
+           (uint32_t)B * 32 * 4;
 }
 
 // Comparison knob: NAME=0 disables a default-on mode.
@@ -602,6 +692,7 @@ bool make_lplan(const LstmArgs& g, int npad, int sms, LPlan& p)
     p.tiles = (int)((g.R + kTcRows - 1) / kTcRows);
     p.chunks = (int)((g.kwords + kChunkWords - 1) / kChunkWords);
     if ((int64_t)p.tiles * p.chunks > sms) return false;       // one unit per CTA, all co-resident
+    if (p.tiles > kLstmMaxTiles || p.tiles * p.chunks > kLstmMaxCtas) return false;   // mailbox slots
     if (p.chunks > 8) return false;                             // a tile's chunks form one (portable) cluster
     p.Gp = tc_group_passes(g.kwords);
     if (p.Gp < 1) return false;

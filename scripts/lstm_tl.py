@@ -35,3 +35,13 @@ if len(c):
     for fin in (0, 1):
         s = c[np.isin(c[:, 1], r[(r[:, 7] == fin)][:, 1])]
         print(("leader " if fin else "other  ") + "  ".join(f"{n} {np.median(s[:, 3 + i]) / 1.965e3:5.2f}" for i, n in enumerate(names)) + " us after h_full (clock64)")
+x = rec[rec[:, 0] == 9]
+if len(x):
+    for t in range(1, T):
+        pub = x[(x[:, 2] == t - 1) & (x[:, 5] > 0)][:, 5]
+        det = x[x[:, 2] == t]
+        if len(pub) and len(det):
+            p1 = pub.max()
+            print(f"step {t}: publish spread {(pub.max()-pub.min())/1e3:5.2f} us; detect after last publish: "
+                  f"min {(det[:,3].min()-p1)/1e3:5.2f} med {(np.median(det[:,3])-p1)/1e3:5.2f} max {(det[:,3].max()-p1)/1e3:5.2f} us; "
+                  f"poll rounds med {np.median(det[:,4]):.0f} max {det[:,4].max()}")
