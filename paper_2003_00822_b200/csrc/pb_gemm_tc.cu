@@ -727,18 +727,20 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     TWAIT(&bars.a_empty[slot], (uint32_t)(sphase ^ 1), 4);
                     tc_fence_after();
                     const int kind = stored_pair ? (use_lo ? 0 : 1) : 2;
-                    const int sgn = ps == 0 ? (g.offset ? 2 : 1) : 0;   // the sign layer's pass: signed nibbles
+                    // the sign layer's pass: complemented (folded into the mask op at no cost; the
+                    // epilogue adds (o - |S_0|) sum_c x_q)
+                    const uint32_t xm = ps == 0 ? (stored_pair ? 0xAAAAAAAAu : 0xFFFFFFFFu) : 0u;
                     const uint32_t t0 = wtile_s + (uint32_t)st0 * kWTileBytes;
                     const uint32_t t1 = wtile_s + (uint32_t)st1 * kWTileBytes;
                     const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
                     uint64_t* r0 = &bars.w_empty[st0];
                     uint64_t* r1 = &bars.w_empty[st1];
                     if (kind == 0)
-                        convert_pass<0>(t0, t1, swz, dst, sgn, p.dbg, r0, r1, lane);
+                        convert_pass<0>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
                     else if (kind == 1)
-                        convert_pass<1>(t0, t1, swz, dst, sgn, p.dbg, r0, r1, lane);
+                        convert_pass<1>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
                     else
-                        convert_pass<2>(t0, t1, swz, dst, sgn, p.dbg, r0, r1, lane);
+                        convert_pass<2>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
                     tc += ntile;
                     converted = true;
@@ -762,9 +764,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const int m = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer; + the midpoint offset
-        // the midpoint offset 2^(L-k_used-1) sum_c x_q (pb_matmul_ex); the sign layer carries its
-        // own negative weight (signed nibbles), so nothing else needs sum_c x_q
-        const unsigned long long o_corr = g.mid;
+        // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer; + the midpoint offset
+        // 2^(L-k_used-1) sum_c x_q (pb_matmul_ex)
+        const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0, true) + g.mid;
         bool have_xsum = false;
         const int pt = threadIdx.x - kEpi0 * 32;      // 0..127
         const int nd = act_digits(g.a);               // activation digits per batch column
@@ -802,7 +804,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // a5: y = dequant(acc) (+ bias, + y when accumulating), then fn -- or, in cell mode
         // (pb_lstm_seq), the LSTM cell over the 4 gate rows of a hidden unit (lanes 4j..4j+3)
         auto preact = [&](int b, int64_t row, unsigned long long t) -> float {
-            if (o_corr) t += o_corr * xsum_of(b);
+            t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
             const long long accv = (long long)t;
             const int64_t o = (int64_t)b * g.R + row;
             if (g.acc) g.acc[o] = accv;
@@ -937,7 +939,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 for (int r = 0; r < p.regions; ++r) {
                     int last = (r + 1) * p.Gp - 1;
                     if (last > p.passes - 1) last = p.passes - 1;
-                    const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last));
+                    const unsigned long long wr = layer_mag(g.L, g.offset, pass_lo(g.k_used, last), true);
                     const uint32_t dreg = tmem + lane_off + (uint32_t)(p.d_col + (db * p.regions + r) * NPAD);
                     if (!kWide && g.B == 1) {
                         // all of the region's columns in one batch of loads, one wait; digit

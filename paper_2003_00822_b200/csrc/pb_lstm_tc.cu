@@ -259,11 +259,11 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 const uint32_t t1 = wtile_s + (uint32_t)st1 * kWTileBytes;
                 const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
                 if (kind == 0)
-                    convert_pass<0>(t0, t1, swz, dst, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                    convert_pass<0>(t0, t1, swz, dst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
                 else if (kind == 1)
-                    convert_pass<1>(t0, t1, swz, dst, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                    convert_pass<1>(t0, t1, swz, dst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
                 else
-                    convert_pass<2>(t0, t1, swz, dst, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                    convert_pass<2>(t0, t1, swz, dst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
                 tc += ntile;
                 pend_slot = slot;
                 slot += 2;

@@ -160,8 +160,8 @@ __device__ __forceinline__ uint32_t sign_nibbles(uint32_t x, bool binary) {
 // producer before its A registers are built and stored to TMEM (32 columns
 // per 4 chunks).
 template <int KIND>
-__device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, int sgn,
-                                             int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
+__device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
+                                             int sgn, int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
     constexpr bool kPair = KIND <= 1;
 #pragma unroll
     for (int t = 0; t < (kPair ? 2 : 1); ++t) {
@@ -175,10 +175,10 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
             uint32_t v[32];
             if (kPair) {
                 const uint4 qq[4] = {q[4 * h], q[4 * h + 1], q[4 * h + 2], q[4 * h + 3]};
-                build_a<KIND>(qq, 0u, v);
+                build_a<KIND>(qq, xm, v);
             } else {
                 const uint4 qq[4] = {q[2 * h], q[2 * h + 1], q[2 * h], q[2 * h + 1]};
-                build_a<KIND>(qq, 0u, v);
+                build_a<KIND>(qq, xm, v);
             }
             if (sgn) {                          // warp-uniform: pass 0 only
 #pragma unroll
@@ -210,8 +210,10 @@ __device__ __forceinline__ void pass_region_g(int Gp, int passes, int k_used, in
 }
 // |S_i|: 2^(L-1-i), the unit of a pass whose least significant layer is i.  The
 // binary code 1 - 2 W_0 (offset 1) is carried whole by its +-0.5 nibbles: unit 1.
-__device__ __forceinline__ unsigned long long layer_mag(int L, int offset, int i) {
-    if (i == 0 && offset) return 1ull;
+// Complemented sign layer (xm, the tensor engine's batch path): the binary layer's unit is
+// |S_0| = 2, with the correction (o - |S_0|) sum_c x_q in the epilogue.
+__device__ __forceinline__ unsigned long long layer_mag(int L, int offset, int i, bool complement = false) {
+    if (i == 0 && offset) return complement ? 2ull : 1ull;
     return 1ull << (L - 1 - i);
 }
 
