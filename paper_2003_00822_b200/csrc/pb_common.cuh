@@ -40,10 +40,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
+#ifdef PB_WAIT_HINT
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+#else
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+#endif
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
+#ifdef PB_WAIT_HINT
+        , "r"((uint32_t)PB_WAIT_HINT)
+#endif
         : "memory");
 }
 // global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0).

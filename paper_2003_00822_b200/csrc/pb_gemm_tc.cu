@@ -286,19 +286,10 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     }
     asm volatile("bar.sync 5, 128;" ::: "memory");
     if TLP(g) tfb = gtimer();
-    auto transpose2 = [&](long long q0, long long q1, uint32_t& m0, uint32_t& m1) {
-        const uint32_t u0 = (uint32_t)q0, u1 = (uint32_t)q1;
-        m0 = m1 = 0;
-        for (int j = 0; j < g.a; ++j) {
-            const uint32_t bit = 1u << (g.a - 1 - j);
-            const uint32_t w0 = __ballot_sync(0xffffffffu, (u0 & bit) != 0);
-            const uint32_t w1 = __ballot_sync(0xffffffffu, (u1 & bit) != 0);
-            if (lane == j) {
-                m0 = w0;
-                m1 = w1;
-            }
-        }
-    };
+    // even a <= 16: digits by a per-lane nibble transpose (digit_regs_shfl, pb_common.cuh) and
+    // 32-bit stores; otherwise one ballot per plane (digit_of_lane)
+    const bool shfl = !(g.a & 1) && g.a <= 16;
+    const uint32_t amask = g.a >= 32 ? ~0u : ((1u << g.a) - 1u);
     // ---- the CTA's slice of the grid-wide B operand first: warp 2's grid barrier that
     // publishes the slices for the later chunks then overlaps the first chunk's build
     int k = 0;
@@ -308,10 +299,20 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         const uint32_t w = it - b * Wt;
         const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
         const long long q = act_cast(v, bars.f[b], g.a);
-        uint32_t mine, dummy;
-        transpose2(q, 0, mine, dummy);
-        uint4 dv;
-        if (digit_of_lane(mine, lane, g.a, dv)) put_b_operand(g.bexp, NPAD, w, b * nd + (lane >> 1), dv);
+        if (shfl) {
+            int dk;
+            const uint32_t reg = digit_regs_shfl((uint32_t)q & amask, g.a, lane, dk);
+            if (dk < nd)
+                *reinterpret_cast<uint32_t*>(g.bexp + b_operand_offset(NPAD, w, b * nd + dk, lane & 3)) = reg;
+        } else {
+            uint32_t mine = 0;
+            for (int j = 0; j < g.a; ++j) {
+                const uint32_t wj = __ballot_sync(0xffffffffu, ((uint32_t)q >> (g.a - 1 - j)) & 1u);
+                if (lane == j) mine = wj;
+            }
+            uint4 dv;
+            if (digit_of_lane(mine, lane, g.a, dv)) put_b_operand(g.bexp, NPAD, w, b * nd + (lane >> 1), dv);
+        }
         if (b == B - 1)
             for (int n = B * nd + lane; n < NPAD; n += 32) put_b_operand(g.bexp, NPAD, w, n, make_uint4(0, 0, 0, 0));
         long long xs = q;
@@ -329,46 +330,69 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     if TLP(g) ttr = gtimer();
     // warp 2 arrives at the grid barrier for this CTA once its slice is written
     if (et == 0) mbar_arrive(&bars.slice_done);
-    // ---- a1 (part 2) + a2 for the first chunk: cast, ballot-transpose (x_q fits 32 bits:
-    // a <= 32), e2m1 B rows straight into B stage 0
+    // ---- a1 (part 2) + a2 for the first chunk: cast and transpose kCx words per warp at a time
+    // (the words itb + kPW k of batch column itb / 32: no branches inside a group), e2m1 B rows
+    // straight into B stage 0
     const uint32_t bstage0_s = smem_u32(bstage0);
-    auto put0 = [&](int it, uint32_t mine) {
-        const int b = it / kChunkWords, wl = it - b * kChunkWords;
-        uint4 dv;
-        if (digit_of_lane(mine, lane, g.a, dv)) put_b_operand_smem(bstage0_s, NPAD, wl, b * nd + (lane >> 1), dv);
-        if (b == B - 1)
-            for (int n = B * nd + lane; n < NPAD; n += 32)
-                put_b_operand_smem(bstage0_s, NPAD, wl, n, make_uint4(0, 0, 0, 0));
-    };
-    // kCx items (itb + kPW * k) per step: kCx independent ballot chains in flight
     auto chunk_group = [&](int itb, const float (&v)[kCx]) {
-        uint32_t u[kCx], mm[kCx];
+        const int b = itb / kChunkWords;              // kPW * kCx == kChunkWords: one column
+        const int f = bars.f[b];
+        uint32_t u[kCx];
+        if (g.a <= 24 && f >= -126 && f <= 127) {
+            // act_cast's exact fp32 form (pb_common.cuh)
+            const float sc = __int_as_float((127 + f) << 23), lim = (float)(1 << (g.a - 1));
 #pragma unroll
-        for (int k = 0; k < kCx; ++k) {
-            const int it = itb + kPW * k;
-            u[k] = (uint32_t)act_cast(v[k], bars.f[it < nci ? it / kChunkWords : 0], g.a);
-            mm[k] = 0;
+            for (int k = 0; k < kCx; ++k) u[k] = (uint32_t)__float2int_rz(fminf(fmaxf(v[k] * sc, -lim), lim - 1.0f));
+        } else {
+#pragma unroll 1
+            for (int k = 0; k < kCx; ++k) u[k] = (uint32_t)act_cast(v[k], f, g.a);
         }
         const long long c1 = kTimeline ? clock64() : 0;
+        if (shfl) {
+            uint32_t reg[kCx];
+            int dk = 0;
+#pragma unroll
+            for (int k = 0; k < kCx; ++k) reg[k] = digit_regs_shfl(u[k] & amask, g.a, lane, dk);
+            if (dk < nd) {
+#pragma unroll
+                for (int k = 0; k < kCx; ++k)
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(bstage0_s + b_operand_offset(NPAD, itb - b * kChunkWords + kPW * k, b * nd + dk, lane & 3)),
+                                 "r"(reg[k]) : "memory");
+            }
+        } else {
+            uint32_t mm[kCx];
+#pragma unroll
+            for (int k = 0; k < kCx; ++k) mm[k] = 0;
 #pragma unroll 1
-        for (int j = 0; j < g.a; ++j) {
-            const uint32_t bit = 1u << (g.a - 1 - j);
+            for (int j = 0; j < g.a; ++j) {
+                const uint32_t bit = 1u << (g.a - 1 - j);
+#pragma unroll
+                for (int k = 0; k < kCx; ++k) {
+                    const uint32_t w = __ballot_sync(0xffffffffu, (u[k] & bit) != 0);
+                    if (lane == j) mm[k] = w;
+                }
+            }
 #pragma unroll
             for (int k = 0; k < kCx; ++k) {
-                const uint32_t w = __ballot_sync(0xffffffffu, (u[k] & bit) != 0);
-                if (lane == j) mm[k] = w;
+                uint4 dv;
+                if (digit_of_lane(mm[k], lane, g.a, dv))
+                    put_b_operand_smem(bstage0_s, NPAD, itb - b * kChunkWords + kPW * k, b * nd + (lane >> 1), dv);
             }
         }
         const long long c2 = kTimeline ? clock64() : 0;
-#pragma unroll
-        for (int k = 0; k < kCx; ++k)
-            if (itb + kPW * k < nci) put0(itb + kPW * k, mm[k]);
+        if (b == B - 1 && B * nd < NPAD) {
+#pragma unroll 1
+            for (int k = 0; k < kCx; ++k)
+                for (int n = B * nd + lane; n < NPAD; n += 32)
+                    put_b_operand_smem(bstage0_s, NPAD, itb - b * kChunkWords + kPW * k, n, make_uint4(0, 0, 0, 0));
+        }
         if (kTimeline) {
             cyc_ballot += c2 - c1;
             cyc_put += clock64() - c2;
         }
     };
-    chunk_group(pw, cx);                               // warp-uniform bounds (ballots inside)
+    static_assert(kPW * kCx == kChunkWords, "a chunk group covers one batch column");
+    chunk_group(pw, cx);
 #pragma unroll 1
     for (int itb = pw + kPW * kCx; itb < nci; itb += kPW * kCx) {
         float v[kCx];
