@@ -344,7 +344,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
 #pragma unroll
             for (int k = 0; k < kCx; ++k) u[k] = (uint32_t)__float2int_rz(fminf(fmaxf(v[k] * sc, -lim), lim - 1.0f));
         } else {
-#pragma unroll 1
+#pragma unroll   // (indexed registers: no local-memory array)
             for (int k = 0; k < kCx; ++k) u[k] = (uint32_t)act_cast(v[k], f, g.a);
         }
         const long long c1 = kTimeline ? clock64() : 0;

@@ -478,7 +478,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                         u[k] = (uint32_t)__float2int_rz(fminf(fmaxf(v[k] * sc, -lim), lim - 1.0f));
                 } else {
                     const int f = bars.f[par][b];
-#pragma unroll 1
+#pragma unroll   // (indexed registers: no local-memory array)
                     for (int k = 0; k < 8; ++k) u[k] = (uint32_t)act_cast(v[k], f, a);
                 }
                 if (g.tl && b == 0) {
