@@ -220,6 +220,14 @@ __device__ __forceinline__ void lstm_cell(float gi, float gf, float gg, float go
     c_out = cn;
     h_out = sigmoidf_(go) * tanhf(cn);
 }
+// The same from the gates' activations (sigmoid(i), sigmoid(f), tanh(g), sigmoid(o)), each
+// computed by the lane that holds its gate.
+__device__ __forceinline__ void lstm_cell_act(float si, float sf, float tg, float so, float c, float& h_out,
+                                              float& c_out) {
+    const float cn = sf * c + si * tg;
+    c_out = cn;
+    h_out = so * tanhf(cn);
+}
 __device__ __forceinline__ float apply_fn(float v, int fn) {
     switch (fn) {
         case 1: return v > 0.f ? v : 0.f;

@@ -91,6 +91,8 @@ struct LPlan {
     int slots, sf_col, d_col, wstages;
     int passes, Gp, regions;
     int resident;              // the unit's A (all passes) stays in TMEM for every timestep
+    int helpers;               // resident, B = 1, even a <= 16: the converter warps build the
+                               // digits of steps t >= 1 (with their A converted once, they idle)
 };
 
 template <int NPAD>
@@ -273,6 +275,64 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 }
             }
         publish();
+        if (p.helpers && T > 1) {
+            // ---- steps t >= 1: this warp's 4 words (cw + 8k) of the CTA's K-chunk of h_t, polled
+            //      as tagged values (the epilogue warps poll the max slots meanwhile), then cast
+            //      with f_b (named barrier 2) and transposed into the B operand (barrier 3)
+            pdl_wait();
+            const unsigned long long sbase = ld_acquire_gpu_u64(g.stepctr);
+            const int H = (int)g.H, a = g.a, nd = act_digits(a);
+            const int cbase = kc * kChunkWords * 32, cvalid = H - cbase;
+            const uint32_t bstage_s = smem_u32(bstage);
+            const uint32_t amask = (1u << a) - 1u;
+            const float lim = (float)(1 << (a - 1));
+            for (int t = 1; t < T; ++t) {
+                const int par = t & 1;
+                const uint32_t tag = (uint32_t)(sbase + (unsigned long long)t);
+                const unsigned long long* hx = g.hx + (int64_t)par * H + cbase;
+                unsigned long long hv[4];
+                bool ok;
+                do {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int cl = (cw + 8 * k) * 32 + lane;
+                        hv[k] = cl < cvalid ? ld_relaxed_gpu_u64(hx + cl) : (unsigned long long)tag << 32;
+                    }
+                    ok = true;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) ok = ok && (uint32_t)(hv[k] >> 32) == tag;
+                } while (!ok);
+                asm volatile("bar.sync 2, 384;" ::: "memory");          // f_b of step t in bars
+                uint32_t u[4], reg[4];
+                if (bars.scl[par][0] != 0.f) {
+                    const float sc = bars.scl[par][0];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        u[k] = (uint32_t)__float2int_rz(fminf(fmaxf(__uint_as_float((uint32_t)hv[k]) * sc, -lim), lim - 1.0f));
+                } else {
+                    const int f = bars.f[par][0];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) u[k] = (uint32_t)act_cast(__uint_as_float((uint32_t)hv[k]), f, a);
+                }
+                int dk = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) reg[k] = digit_regs_shfl(u[k] & amask, a, lane, dk);
+                if (dk < nd) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(bstage_s + b_operand_offset(NPAD, cw + 8 * k, dk, lane & 3)),
+                                     "r"(reg[k]) : "memory");
+                }
+                if (nd < NPAD) {
+#pragma unroll 1
+                    for (int k = 0; k < 4; ++k)
+                        for (int n = nd + lane; n < NPAD; n += 32)
+                            put_b_operand_smem(bstage_s, NPAD, cw + 8 * k, n, make_uint4(0, 0, 0, 0));
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA
+                asm volatile("bar.sync 3, 384;" ::: "memory");          // B of step t complete
+            }
+        }
     } else if (warp == 2) {
         // ---------------------------------------------- step gate: the tile's gx[t] rows (leader),
         // and for B > 1: once h_t is complete on every CTA (grid barrier of step t-1), this CTA's
@@ -346,8 +406,8 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
         // diagnostics: 3 records per step at indices reserved once (no atomic inside the steps)
         long long* tlb = nullptr;
         if (g.tl && pt == 0) {
-            const unsigned long long i0 = atomicAdd(reinterpret_cast<unsigned long long*>(g.tl), 3ull * T);
-            if (i0 + 3ull * T <= (unsigned long long)kTlRecords) tlb = g.tl + 10 + 10 * (long long)i0;
+            const unsigned long long i0 = atomicAdd(reinterpret_cast<unsigned long long*>(g.tl), 4ull * T);
+            if (i0 + 4ull * T <= (unsigned long long)kTlRecords) tlb = g.tl + 10 + 10 * (long long)i0;
         }
         // the cell state of the leader's 32 hidden units stays in SMEM across timesteps
         if (finish && (lane & 3) == 0 && row < R)
@@ -356,6 +416,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             const int par = t & 1;
             long long tm[6] = {0, 0, 0, 0, 0, 0};
             long long ck[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            long long cgx = 0, cfin[3] = {0, 0, 0};
             if (g.tl) tm[0] = gtimer();
             // ---- a1: f_b from max|h_t[b,:]| (reading G8).  Step 0 reads all of h0.  For t > 0 the
             //      CTAs that produced h_t published its maxima: B = 1 per-tile tagged slots, read
@@ -392,6 +453,30 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     bars.scl[0][pt] = (f >= -126 && f <= 127) ? __int_as_float((127 + f) << 23) : 0.f;
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
+            } else if (p.helpers) {
+                // the converter warps poll h_t and build the digits; here: the tiles' max slots
+                const uint32_t tag = (uint32_t)(sbase + (unsigned long long)t);
+                const unsigned long long* sl = g.mxs + ((int64_t)par * gridDim.x + blockIdx.x) * kLstmMaxTiles;
+                unsigned long long sv = (unsigned long long)tag << 32;
+                if (pt < p.tiles) {
+                    sv = ld_relaxed_gpu_u64(sl + pt);
+                    while ((uint32_t)(sv >> 32) != tag) sv = ld_relaxed_gpu_u64(sl + pt);
+                }
+                const float mx = __uint_as_float(__reduce_max_sync(0xffffffffu, (uint32_t)sv));
+                if (lane == 0) bars.red[ew][0] = mx;
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (pt == 0) {
+                    const float m4 = fmaxf(fmaxf(bars.red[0][0], bars.red[1][0]), fmaxf(bars.red[2][0], bars.red[3][0]));
+                    const int f = act_frac_of(m4, a);
+                    bars.f[par][0] = f;
+                    bars.sc[par][0] = col_scale(g.scale, f);
+                    bars.scl[par][0] = (f >= -126 && f <= 127) ? __int_as_float((127 + f) << 23) : 0.f;
+                }
+                if (g.tl) {
+                    tm[4] = gtimer();
+                    tm[5] = 1;
+                }
+                asm volatile("bar.sync 2, 384;" ::: "memory");          // f_b to the converter warps
             } else if (tagx) {
                 const uint32_t tag = (uint32_t)(sbase + (unsigned long long)t);
                 const unsigned long long* hx = g.hx + (int64_t)par * H + cbase;
@@ -456,8 +541,9 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             const bool shfl_digits = !(a & 1) && a <= 16;
             const uint32_t amask = a >= 32 ? ~0u : ((1u << a) - 1u);
             static_assert(kEpiWarps * 8 == kChunkWords, "a round covers one batch column");
+            const bool helped = p.helpers && t > 0;       // the converter warps built the digits
 #pragma unroll 1
-            for (int b = 0; b < B; ++b) {
+            for (int b = 0; b < (helped ? 0 : B); ++b) {
                 uint32_t u[8];
                 float v[8];
                 if (tagx) {
@@ -520,7 +606,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     }
                 }
             }
-            if (B * nd < NPAD) {                               // zero digit rows past the batch
+            if (B * nd < NPAD && !helped) {                    // zero digit rows past the batch
 #pragma unroll 1
                 for (int k = 0; k < 8; ++k)
                     for (int n = B * nd + lane; n < NPAD; n += 32)
@@ -528,7 +614,10 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             }
             if (g.tl) ck[1] = clock64();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (helped)
+                asm volatile("bar.sync 3, 384;" ::: "memory");           // the converter warps' digits
+            else
+                asm volatile("bar.sync 1, 128;" ::: "memory");
             if (g.tl) ck[2] = clock64();
             if (pt == 0) {
                 mbar_arrive(&bars.b_full);
@@ -605,19 +694,28 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 unsigned long long* hx1 = g.hx + (int64_t)((t + 1) & 1) * H;
                 mbar_wait(&bars.gx_full[t & 1], (uint32_t)((t >> 1) & 1));
                 if (g.tl) ck[6] = clock64();
+                if (g.tl) cgx = ck[6];
+                long long cf[3] = {0, 0, 0};
                 for (int b = 0; b < B; ++b) {
                     unsigned long long tt = tot_of(b);
                     for (int r = 1; r < p.chunks; ++r)
                         tt += ld_shared_u64(redbuf_s + (uint32_t)((((r - 1) * B + b) * kTcRows + m) * 8));
                     const float v = row < R ? dequant_sc((long long)tt, bars.sc[par][b]) + gxbuf[(par * B + b) * kTcRows + m] : 0.f;
+                    if (g.tl && b == 0) {
+                        asm volatile("" ::"f"(v));
+                        cf[0] = clock64();
+                    }
+                    // each gate lane applies its own nonlinearity (tanh for g, sigmoid else), then
+                    // the unit's lane gathers the four activations
+                    const float act = (lane & 3) == 2 ? tanhf(v) : sigmoidf_(v);
                     const int q0 = lane & ~3;
-                    const float gi = __shfl_sync(0xffffffffu, v, q0), gf = __shfl_sync(0xffffffffu, v, q0 + 1);
-                    const float gg = __shfl_sync(0xffffffffu, v, q0 + 2), go = __shfl_sync(0xffffffffu, v, q0 + 3);
+                    const float si = __shfl_sync(0xffffffffu, act, q0), sf = __shfl_sync(0xffffffffu, act, q0 + 1);
+                    const float tg = __shfl_sync(0xffffffffu, act, q0 + 2), so = __shfl_sync(0xffffffffu, act, q0 + 3);
                     float hn = 0.f;
                     if ((lane & 3) == 0 && row < R) {
                         const int64_t i = (int64_t)b * H + (row >> 2);
                         float cn;
-                        lstm_cell(gi, gf, gg, go, cst[b * 32 + (m >> 2)], hn, cn);
+                        lstm_cell_act(si, sf, tg, so, cst[b * 32 + (m >> 2)], hn, cn);
                         cst[b * 32 + (m >> 2)] = cn;
                         if (tagx && t + 1 < T)
                             st_relaxed_gpu_u64(hx1 + (row >> 2), ((unsigned long long)tag1 << 32) | __float_as_uint(hn));
@@ -625,10 +723,20 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                         if (g.c_seq) g.c_seq[(int64_t)t * B * H + i] = cn;
                         if (t == T - 1) g.c_last[i] = cn;
                     }
-                    // max|h_{t+1}[b,:]| over this warp's 8 hidden units -> step t+1's f_b
-                    float mh = fabsf(hn);
-#pragma unroll
-                    for (int o = 16; o; o >>= 1) mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+                    if (g.tl && b == 0) {
+                        asm volatile("" ::"f"(hn));
+                        cf[1] = clock64();
+                    }
+                    // max|h_{t+1}[b,:]| over this warp's 8 hidden units -> step t+1's f_b (non-negative
+                    // floats order as their bit patterns: one redux)
+                    const float mh = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(fabsf(hn))));
+                    if (g.tl && b == 0) {
+                        asm volatile("" ::"f"(mh));
+                        cf[2] = clock64();
+                        cfin[0] = cf[0];
+                        cfin[1] = cf[1];
+                        cfin[2] = cf[2];
+                    }
                     if (lane == 0 && t + 1 < T) {
                         if (tagx)
                             bars.pmax[par][ew] = mh;
@@ -654,13 +762,14 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 if (g.tl && pt == 0) ck[6] = gtimer();
             }
             if (tlb) {
-                long long* rr = tlb + 30 * t;
-                const long long rec[30] = {7, blockIdx.x, t, tm[0], tm[1], tm[2], tm[3], finish ? 1 : 0, gtimer(), 0,
+                long long* rr = tlb + 40 * t;
+                const long long rec[40] = {7, blockIdx.x, t, tm[0], tm[1], tm[2], tm[3], finish ? 1 : 0, gtimer(), 0,
                                            8, blockIdx.x, t, ck[1] - ck[0], ck[2] - ck[0], ck[3] - ck[0], ck[4] - ck[0],
                                            ck[5] - ck[0], ck[8] - ck[0], ck[7] - ck[0],
-                                           9, blockIdx.x, t, tm[4], tm[5], finish ? ck[6] : 0, 0, 0, 0, 0};
+                                           9, blockIdx.x, t, tm[4], tm[5], finish ? ck[6] : 0, 0, 0, 0, 0,
+                                           10, blockIdx.x, t, cgx - ck[0], cfin[0] - ck[0], cfin[1] - ck[0], cfin[2] - ck[0], 0, 0, 0};
 #pragma unroll
-                for (int k = 0; k < 30; ++k) rr[k] = rec[k];
+                for (int k = 0; k < 40; ++k) rr[k] = rec[k];
             }
         }
         // the next call's tags start past this call's: CTA 0 advances the step counter
@@ -706,6 +815,7 @@ bool make_lplan(const LstmArgs& g, int npad, int sms, LPlan& p)
     // A of every pass resident (converted once, at step 0) when it fits the A ring
     p.resident = (p.passes <= p.slots && !getenv_flag_off("PB_LSTM_RESIDENT")) ? 1 : 0;
     if (p.resident) p.slots = p.passes;
+    p.helpers = (p.resident && g.B == 1 && !(g.a & 1) && g.a <= 16 && !getenv_flag_off("PB_LSTM_HELPERS")) ? 1 : 0;
     p.wstages = (int)((kSmemMax - lstm_fixed_smem(g.B, npad, p.chunks)) / kWTileBytes);
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     // >= 4: the two converter h-sets wait on the tiles of consecutive passes (2 tiles each); with

@@ -45,3 +45,8 @@ if len(x):
             print(f"step {t}: publish spread {(pub.max()-pub.min())/1e3:5.2f} us; detect after last publish: "
                   f"min {(det[:,3].min()-p1)/1e3:5.2f} med {(np.median(det[:,3])-p1)/1e3:5.2f} max {(det[:,3].max()-p1)/1e3:5.2f} us; "
                   f"poll rounds med {np.median(det[:,4]):.0f} max {det[:,4].max()}")
+z = rec[(rec[:, 0] == 10) & (rec[:, 2] > 0)]
+z = z[z[:, 3] > 0]
+if len(z):
+    print("leader finalisation (us after h_full, clock64): gx " + "  ".join(
+        f"{n} {np.median(z[:, 3 + i]) / 1.965e3:5.2f}" for i, n in enumerate(["gx", "dequant", "cell", "max"])))
