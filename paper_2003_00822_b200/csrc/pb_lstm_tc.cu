@@ -134,7 +134,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
         mbar_init(&bars.d_empty, kEpiWarps);
         mbar_init(&bars.h_full, 2);                // the copies (expect_tx) + f_b of the step
         mbar_init(&bars.h_empty, 1);
-        mbar_init(&bars.red_full, p.chunks > 1 ? p.chunks - 1 : 1);
+        mbar_init(&bars.red_full, 1);              // the leader's expect_tx; the others' st.async bytes
         mbar_init(&bars.gx_full[0], 1);
         mbar_init(&bars.gx_full[1], 1);
         fence_mbar_init();
@@ -414,6 +414,8 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             for (int b = 0; b < B; ++b) cst[b * 32 + (m >> 2)] = g.c0[(int64_t)b * H + (row >> 2)];
         for (int t = 0; t < T; ++t) {
             const int par = t & 1;
+            if (finish && p.chunks > 1 && pt == 0)                 // this step's partial sums from the others
+                mbar_arrive_expect_tx(&bars.red_full, (uint32_t)((p.chunks - 1) * B * kTcRows * 8));
             long long tm[6] = {0, 0, 0, 0, 0, 0};
             long long ck[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
             long long cgx = 0, cfin[3] = {0, 0, 0};
@@ -680,10 +682,14 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             // ---- a5: a tile's K-chunks are the CTAs of one cluster: the others put their exact
             //      partial sums into the leader's SMEM (DSMEM) and the leader finishes the tile
             if (!finish) {
+                // every thread's sums go with their byte count to the leader's barrier (st.async)
                 const uint32_t rb = mapa_shared(redbuf_s + (uint32_t)(((kc - 1) * B * kTcRows + m) * 8), 0);
-                for (int b = 0; b < B; ++b) st_cluster_u64(rb + (uint32_t)(b * kTcRows * 8), tot_of(b));
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (pt == 0) mbar_arrive_cluster(mapa_shared(smem_u32(&bars.red_full), 0));
+                const uint32_t rbar = mapa_shared(smem_u32(&bars.red_full), 0);
+                for (int b = 0; b < B; ++b)
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                                     rb + (uint32_t)(b * kTcRows * 8)),
+                                 "l"(tot_of(b)), "r"(rbar)
+                                 : "memory");
             } else if (p.chunks > 1) {
                 mbar_wait_cluster(&bars.red_full, (uint32_t)(t & 1));
             }
