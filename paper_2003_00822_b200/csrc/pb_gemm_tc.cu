@@ -1342,6 +1342,13 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
         p.Gu = 1;
         p.ustat = p.units - dyn;
         if (p.ustat < p.gs) p.ustat = p.units < p.gs ? p.units : p.gs;
+        // wide mode with few (slice, tile) pairs: one whole tile per CTA, so no tile is shared
+        // and no partial sums go through atomics (the wide epilogue's dominant cost: 16
+        // batch columns x 128 rows per shared tile)
+        if (NPAD > kTcMaxN && p.chunks > 1 && (long long)p.slices * p.tiles <= sms && !dyn) {
+            p.gs = (int)(p.slices * p.tiles);
+            p.ustat = p.units;
+        }
         p.items = p.gs + (p.units - p.ustat);
     }
     CUtensorMap pmap, smap;
