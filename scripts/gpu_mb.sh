@@ -1,5 +1,7 @@
 #!/bin/bash
-# microbenchmarks + a quick bench line (scratch runs; results land in gpurun_out/)
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mxf4_mb scripts/mxf4_mb.cu && timeout 120 /tmp/mxf4_mb > gpurun_out/mxf4_mb.txt 2>&1
-python build_pb.py > /dev/null
-timeout 600 python bench.py --steps 200 --warmup 10 --no-sweep --no-compare --no-lstm --no-cpu > gpurun_out/bench_quick.json 2> gpurun_out/bench_quick.err
+# microbenchmarks behind DESIGN.md §6 (MMA issue rate, TMEM stores, TMA tile streaming, PDL)
+mkdir -p gpurun_out
+for mb in mxf4_mb tc_mb tma_mb pdl_probe tc_probe_2cta; do
+  nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/$mb scripts/$mb.cu && timeout -s KILL 120 /tmp/$mb > gpurun_out/$mb.txt 2>&1
+  echo "$mb rc=$?"
+done
