@@ -788,7 +788,6 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         const int m = q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer; + the midpoint offset
-        // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer; + the midpoint offset
         // 2^(L-k_used-1) sum_c x_q (pb_matmul_ex)
         const unsigned long long o_corr = (unsigned long long)g.offset - layer_mag(g.L, g.offset, 0, true) + g.mid;
         bool have_xsum = false;
