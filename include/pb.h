@@ -169,13 +169,16 @@ pb_status pb_search_clip(const float* W_host, int64_t rows, int64_t cols, int32_
  *   [work counters int32 x 2]                 zero on entry, left zero
  *   [end barrier uint64]                      monotonic arrival counter
  *   [tensor-engine partial-tile sums int64 x 2048 x S x 128, S = the largest
- *    batch slice of one launch for this act_bits, min(32, 64 / act_bits)]
+ *    batch slice of one narrow launch for this act_bits, min(32, 64 / ceil(act_bits/2))]
  *                                             zero on entry, left zero
  *   [f_b int32 x batch][x_q partial sums int64 x batch x 160]
  *   [planes uint32 x batch x act_bits x kwords]
- *   [tensor-engine B operand tiles of one launch's batch slice: roundup(kwords, 32)
- *    x N_pad x 16 bytes, N_pad = a * slice padded to 8/16/32/64; slice = batch
- *    when a*batch <= 64 and batch <= 32, else min(32, 64/a) columns]
+ *   [tensor-engine B operand tiles (activation planes stacked in pairs: ceil(a/2)
+ *    digit rows per batch column): narrow, roundup(kwords, 32) x N_pad x 16 bytes,
+ *    N_pad = ceil(a/2) * slice padded to 8/16/32/64, slice = batch when
+ *    ceil(a/2)*batch <= 64 and batch <= 32, else min(32, 64/ceil(a/2)) columns;
+ *    wide mode (larger batches): slice-major 128-row tiles, one slice per
+ *    128/ceil(a/2) batch columns, every slice of the batch]
  * each region 256-byte aligned.  The workspace must be zero-filled before its
  * first use (the counters); every other region is rewritten by each call, so
  * one workspace serves calls of any shape with the same act_bits (the
@@ -264,9 +267,14 @@ pb_status pb_lstm_step(const float* x_t, const float* h, const float* c,
  *   1. gx[t][b] = W_ih x[t][b] + bias for all steps*batch columns in one
  *      batched call (the input projection hoisted out of the recurrence);
  *   2. per t: pre = W_hh h_t + gx[t]; c_{t+1} = sigmoid(f) c_t + sigmoid(i) tanh(g),
- *      h_{t+1} = sigmoid(o) tanh(c_{t+1}) -- ONE fused tensor-engine launch
- *      (a1-a5 + the cell in the finalisation, which holds the 4 gate rows of
- *      a unit in adjacent lanes), else planes + GEMM + a cell kernel.
+ *      h_{t+1} = sigmoid(o) tanh(c_{t+1}).  When W_hh's (128-row tile, 1024-column
+ *      chunk) units fit the SMs at once (H <= 2048, batch <= 32), ALL steps run in
+ *      ONE persistent tensor-engine launch (a1-a5 + the cell per step; h exchanged
+ *      between CTAs through the workspace, tagged by a workspace step counter that
+ *      grows by `steps` per call); else one fused launch per step (the cell in the
+ *      finalisation, which holds the 4 gate rows of a unit in adjacent lanes), or
+ *      planes + GEMM + a cell kernel.  The workspace must be zero-filled before its
+ *      first use and is not shared by concurrent calls.
  *   x      device [steps][batch][E];  h0, c0 device [batch][H];
  *   bias   device [4H] (b_ih + b_hh, interleaved) or NULL;
  *   h_seq  device [steps][batch][H]: h_1 .. h_steps (required);
