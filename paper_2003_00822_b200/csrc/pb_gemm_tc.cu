@@ -493,10 +493,10 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     // streaming now, while the other warps wait for the TMEM allocation and the scale factors
     if (warp == 0) {
         __syncwarp();
-        asm volatile("bar.arrive 8, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("barrier.arrive 8, %0;" ::"n"(kThreads) : "memory");   // non-aligned (different code than bar 8 sync)
     } else {
         tc_fence_before();
-        asm volatile("bar.sync 8, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("barrier.sync 8, %0;" ::"n"(kThreads) : "memory");
         tc_fence_after();
     }
     const uint32_t tmem = warp == 0 ? 0u : bars.tmem_base;

@@ -302,7 +302,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
 #pragma unroll
                     for (int k = 0; k < 4; ++k) ok = ok && (uint32_t)(hv[k] >> 32) == tag;
                 } while (!ok);
-                asm volatile("bar.sync 2, 384;" ::: "memory");          // f_b of step t in bars
+                asm volatile("barrier.sync 2, 384;" ::: "memory");   // f_b of step t in bars (non-aligned: two code sites)
                 uint32_t u[4], reg[4];
                 if (bars.scl[par][0] != 0.f) {
                     const float sc = bars.scl[par][0];
@@ -330,7 +330,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                             put_b_operand_smem(bstage_s, NPAD, cw + 8 * k, n, make_uint4(0, 0, 0, 0));
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA
-                asm volatile("bar.sync 3, 384;" ::: "memory");          // B of step t complete
+                asm volatile("barrier.sync 3, 384;" ::: "memory");          // B of step t complete
             }
         }
     } else if (warp == 2) {
@@ -478,7 +478,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                     tm[4] = gtimer();
                     tm[5] = 1;
                 }
-                asm volatile("bar.sync 2, 384;" ::: "memory");          // f_b to the converter warps
+                asm volatile("barrier.sync 2, 384;" ::: "memory");   // f_b to the converter warps (non-aligned)
             } else if (tagx) {
                 const uint32_t tag = (uint32_t)(sbase + (unsigned long long)t);
                 const unsigned long long* hx = g.hx + (int64_t)par * H + cbase;
@@ -617,7 +617,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             if (g.tl) ck[1] = clock64();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic SMEM writes -> MMA
             if (helped)
-                asm volatile("bar.sync 3, 384;" ::: "memory");           // the converter warps' digits
+                asm volatile("barrier.sync 3, 384;" ::: "memory");           // the converter warps' digits
             else
                 asm volatile("bar.sync 1, 128;" ::: "memory");
             if (g.tl) ck[2] = clock64();
