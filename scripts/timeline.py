@@ -15,6 +15,7 @@ ap.add_argument("--L", type=int, default=8)
 ap.add_argument("--k-used", type=int, default=0)
 ap.add_argument("--B", type=int, default=1)
 ap.add_argument("--calls", type=int, default=4)
+ap.add_argument("--copies", type=int, default=2, help="weight copies rotated over (1: L2-hot when it fits)")
 ap.add_argument("--out", default="gpurun_out/tl.npy")
 ap.add_argument("--time", type=int, default=0, help="replay the graph this many times and print us per call")
 args = ap.parse_args()
@@ -22,7 +23,7 @@ k_used = args.k_used or args.L
 rng = np.random.default_rng(1)
 codes = rng.integers(-(1 << (args.L - 1)), 1 << (args.L - 1), size=(args.R, args.K), dtype=np.int32)
 w0 = pb.PackedWeights.from_codes(codes, args.L)
-ws_ = [w0] + [w0.clone_to(torch.empty_like(w0.buf)) for _ in range(1)]
+ws_ = [w0] + [w0.clone_to(torch.empty_like(w0.buf)) for _ in range(args.copies - 1)]
 x = torch.randn(args.B, args.K, device="cuda")
 ws = pb.Workspace(pb.workspace_bytes(args.B, args.K, 16))
 y = torch.empty(args.B, args.R, device="cuda")

@@ -21,7 +21,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
 // ORDER 1: the GEMM's order -- per (row tile, k chunk) unit all L layers, units contiguous per CTA.
 template <int STAGES, int BOXW, int BOXR, int ORDER>
 __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensorMap map, int kwords, int R, int L,
-                                                 int* out) {
+                                                 int* out, int reps = 1) {
     extern __shared__ __align__(1024) uint8_t smraw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensor
     const long long t0 = total * blockIdx.x / gridDim.x, t1 = total * (blockIdx.x + 1) / gridDim.x;
     if (warp == 0 && lane == 0) {
         int n = 0;
+        for (int rp = 0; rp < reps; ++rp)
         for (long long t = t0; t < t1; ++t, ++n) {
             const int st = n % STAGES;
             mbar_wait(&empty[st], ((n / STAGES) & 1) ^ 1);
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensor
     } else if (warp == 1 && lane == 0) {
         int n = 0;
         uint32_t acc = 0;
+        for (int rp = 0; rp < reps; ++rp)
         for (long long t = t0; t < t1; ++t, ++n) {
             const int st = n % STAGES;
             mbar_wait(&full[st], (n / STAGES) & 1);
@@ -76,12 +78,78 @@ __global__ void __launch_bounds__(64, 1) stream(const __grid_constant__ CUtensor
     }
 }
 
+
+// 1-D bulk copies (cp.async.bulk, no tensor map) of contiguous TILE-byte blocks: the rate of a
+// pre-tiled weight layout.  Each CTA streams its contiguous share `reps` times.
+template <int STAGES, int TILE>
+__global__ void __launch_bounds__(64, 1) stream1d(const uint8_t* src, long long bytes, int* out, int reps) {
+    extern __shared__ __align__(1024) uint8_t smraw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    const long long total = bytes / TILE;
+    const long long t0 = total * blockIdx.x / gridDim.x, t1 = total * (blockIdx.x + 1) / gridDim.x;
+    if (warp == 0 && lane == 0) {
+        int n = 0;
+        for (int rp = 0; rp < reps; ++rp)
+            for (long long t = t0; t < t1; ++t, ++n) {
+                const int st = n % STAGES;
+                mbar_wait(&empty[st], ((n / STAGES) & 1) ^ 1);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[st])), "r"(TILE)
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 smem_u32(sm + st * TILE)),
+                             "l"(src + t * TILE), "r"(TILE), "r"(smem_u32(&full[st]))
+                             : "memory");
+            }
+    } else if (warp == 1 && lane == 0) {
+        int n = 0;
+        uint32_t acc = 0;
+        for (int rp = 0; rp < reps; ++rp)
+            for (long long t = t0; t < t1; ++t, ++n) {
+                const int st = n % STAGES;
+                mbar_wait(&full[st], (n / STAGES) & 1);
+                acc += *reinterpret_cast<volatile uint32_t*>(sm + st * TILE + (n & 127) * 4);
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[st])) : "memory");
+            }
+        if (acc == 0x12345678) out[0] = 1;
+    }
+}
+template <int STAGES, int TILE>
+void run1d(const uint8_t* buf, long long bytes, int reps) {
+    int* d;
+    cudaMalloc(&d, 4);
+    const size_t smem = STAGES * TILE + 1024;
+    cudaFuncSetAttribute(stream1d<STAGES, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    for (int i = 0; i < 3; ++i) stream1d<STAGES, TILE><<<148, 64, smem>>>(buf, bytes, d, reps);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    const int it = 10;
+    for (int i = 0; i < it; ++i) stream1d<STAGES, TILE><<<148, 64, smem>>>(buf, bytes, d, reps);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("1d reps %2d stages %2d tile %6d B (%.1f MB): %.1f us  %.0f GB/s  %s\n", reps, STAGES, TILE, bytes / 1e6,
+           ms * 1e3 / it, (double)bytes * reps / (ms * 1e-3 / it) / 1e9, cudaGetErrorString(cudaGetLastError()));
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 template <int STAGES, int BOXW, int BOXR, int ORDER = 0>
-void run(void* buf, int kwords, int R, int L) {
+void run(void* buf, int kwords, int R, int L, int reps = 1) {
     static EncodeTiledFn enc = nullptr;
     if (!enc) {
         cudaDriverEntryPointQueryResult q;
@@ -99,19 +167,19 @@ void run(void* buf, int kwords, int R, int L) {
     cudaMalloc(&d, 4);
     const size_t smem = STAGES * BOXW * BOXR * 4 + 1024;
     cudaFuncSetAttribute(stream<STAGES, BOXW, BOXR, ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    for (int i = 0; i < 3; ++i) stream<STAGES, BOXW, BOXR, ORDER><<<148, 64, smem>>>(map, kwords, R, L, d);
+    for (int i = 0; i < 3; ++i) stream<STAGES, BOXW, BOXR, ORDER><<<148, 64, smem>>>(map, kwords, R, L, d, reps);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
     const int it = 10;
-    for (int i = 0; i < it; ++i) stream<STAGES, BOXW, BOXR, ORDER><<<148, 64, smem>>>(map, kwords, R, L, d);
+    for (int i = 0; i < it; ++i) stream<STAGES, BOXW, BOXR, ORDER><<<148, 64, smem>>>(map, kwords, R, L, d, reps);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double bytes = (double)kwords * 4 * R * L;
-    printf("order %d stages %2d box %3dx%3d (%5d B): %.1f us  %.0f GB/s  %s\n", ORDER, STAGES, BOXW, BOXR, BOXW * BOXR * 4,
+    const double bytes = (double)kwords * 4 * R * L * reps;
+    printf("reps %d order %d stages %2d box %3dx%3d (%5d B): %.1f us  %.0f GB/s  %s\n", reps, ORDER, STAGES, BOXW, BOXR, BOXW * BOXR * 4,
            ms * 1e3 / it, bytes / (ms * 1e-3 / it) / 1e9, cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -125,5 +193,17 @@ int main() {
     run<12, 32, 128, 1>(buf, kwords, R, L);
     run<8, 32, 128, 0>(buf, kwords, R, L);
     run<8, 32, 128, 1>(buf, kwords, R, L);
+    // L2-resident (33.5 MB, streamed 8 times per launch): the TMA box rate without HBM
+    run<8, 32, 128, 1>(buf, kwords, R, 2, 8);
+    run<12, 32, 128, 1>(buf, kwords, R, 2, 8);
+    run<12, 32, 64, 1>(buf, kwords, R, 2, 8);
+    run<12, 32, 32, 1>(buf, kwords, R, 2, 8);
+    run<12, 32, 128, 1>(buf, kwords, R, 1, 16);
+    const uint8_t* b8 = static_cast<const uint8_t*>(buf);
+    run1d<12, 16384>(b8, 268435456ll, 1);
+    run1d<12, 16384>(b8, 33554432ll, 8);
+    run1d<12, 8192>(b8, 33554432ll, 8);
+    run1d<6, 32768>(b8, 33554432ll, 8);
+    run1d<12, 16384>(b8, 16777216ll, 16);
     return 0;
 }
