@@ -668,7 +668,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         TWAIT(&bars.a_full[slot], phase, 2);
                         tc_fence_after();
                         if (TLP(g) && t_mma0 == 0) t_mma0 = gtimer();
-                        if (p.dbg == 2 || p.dbg == 3) {
+                        if (p.dbg == 2 || p.dbg == 3 || p.dbg == 4) {
                             if (elect_one()) tc_commit(&bars.a_empty[slot]);
                         } else if (elect_one()) {
                             // descriptor start address advances in 16 B units: one B tile = NPAD*32 B
@@ -1298,6 +1298,8 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     std::call_once(env_once, [] {
         const char* ev = getenv("PB_TC_DEBUG");
         dbg = ev ? atoi(ev) : 0;
+        ev = getenv("PB_TC_KNOB");             // profiling knob with the timeline on (PB_TC_DEBUG=6)
+        if (ev) dbg = atoi(ev);
         ev = getenv("PB_TC_PROF");
         prof = ev ? atoi(ev) : 0;
         ev = getenv("PB_TC_BSTAGES");          // experiment knob: B ring depth

@@ -163,6 +163,14 @@ template <int KIND>
 __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
                                              int sgn, int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
     constexpr bool kPair = KIND <= 1;
+    if (dbg == 4) {                             // profiling knob: the pipeline skeleton only
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(rel0);
+            if (kPair) mbar_arrive(rel1);
+        }
+        return;
+    }
 #pragma unroll
     for (int t = 0; t < (kPair ? 2 : 1); ++t) {
         uint4 q[8];

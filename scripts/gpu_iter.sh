@@ -15,3 +15,4 @@ except Exception as e:
     print("no json", e)
 PY
 if [ -n "$TL" ]; then bash scripts/gpu_tl.sh; fi
+if [ -n "$EXTRA" ]; then bash -c "$EXTRA"; fi
