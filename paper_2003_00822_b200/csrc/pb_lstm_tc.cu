@@ -41,12 +41,13 @@ constexpr int kConv0 = 3;
 constexpr int kEpi0 = kConv0 + kConvWarps;
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 32 * (kEpi0 + kEpiWarps);
-constexpr int kMaxSlots = 4;
+constexpr int kMaxSlots = 4;                  // A slots in TMEM
+constexpr int kMaxSPass = 2;                  // resident passes whose A lives in SMEM (SS MMAs)
 constexpr int kMaxWStages = 16;
 constexpr uint32_t kHdrBytes = 4096;
 
 struct LBars {
-    uint64_t a_full[kMaxSlots], a_empty[kMaxSlots];
+    uint64_t a_full[kMaxSlots + kMaxSPass], a_empty[kMaxSlots];
     uint64_t w_full[kMaxWStages], w_empty[kMaxWStages];
     uint64_t b_full, d_full, d_empty, h_full, h_empty;
     uint64_t red_full;                         // cluster leader: the other chunks' partial sums are in
@@ -90,7 +91,9 @@ struct LPlan {
     int tiles, chunks;
     int slots, sf_col, d_col, wstages;
     int passes, Gp, regions;
-    int resident;              // the unit's A (all passes) stays in TMEM for every timestep
+    int resident;              // the unit's A (all passes) stays on chip for every timestep
+    int spass;                 // resident: the last spass passes keep A in SMEM (64 KiB each, carved
+                               // from the weight ring, idle after step 0; SS MMAs), the rest in TMEM
     int helpers;               // resident, B = 1, even a <= 16: the converter warps build the
                                // digits of steps t >= 1 (with their A converted once, they idle)
 };
@@ -109,7 +112,8 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
     constexpr uint32_t kBStage = (kChunkWords / 2) * kBTile;
     constexpr bool kWide = NPAD > kTcMaxN;
     uint8_t* wtile0 = smem + kHdrBytes;
-    uint8_t* bstage = wtile0 + p.wstages * kWTileBytes;
+    uint8_t* sa = wtile0 + p.wstages * kWTileBytes;            // [spass][16 MMAs][4 KiB] SMEM A
+    uint8_t* bstage = sa + (size_t)p.spass * 16 * 4096;
     const uint32_t s_tot_s = smem_u32(bstage + kBStage);       // [b][128] u64 (B > 1)
     uint8_t* hbuf = bstage + kBStage + (size_t)g.B * kTcRows * 8;  // [b][1024] fp32: the K-chunk of h_t
     const uint32_t redbuf_s = smem_u32(hbuf + (size_t)g.B * kChunkWords * 32 * 4);   // [chunks-1][b][128] u64
@@ -125,6 +129,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
             mbar_init(&bars.a_full[s], 4);
             mbar_init(&bars.a_empty[s], 1);
         }
+        for (int s = p.slots; s < p.slots + p.spass; ++s) mbar_init(&bars.a_full[s], 4);
         for (int s = 0; s < p.wstages; ++s) {
             mbar_init(&bars.w_full[s], 1);
             mbar_init(&bars.w_empty[s], 4);
@@ -198,14 +203,23 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 const uint32_t dcol = tmem + (uint32_t)(p.d_col + region * NPAD);
                 const uint32_t sfb = tmem + (uint32_t)(p.sf_col + 4 * (1 + sexp));
                 if (p.resident) slot = (uint32_t)ps;
-                if (!p.resident || t == 0) mbar_wait(&bars.a_full[slot], phase);
+                if (!p.resident || t == 0) mbar_wait(&bars.a_full[slot], p.resident ? 0u : phase);
                 tc_fence_after();
                 if (elect_one()) {
-                    const uint32_t a0 = tmem + slot * 128;
+                    if (p.resident && ps >= p.slots) {
+                        // A in SMEM (SS): 16 tiles of 128 rows x 32 B, 4 KiB apart
+                        const uint64_t ad0 = b_desc(smem_u32(sa) + (uint32_t)(ps - p.slots) * 16u * 4096u);
 #pragma unroll
-                    for (int uu = 0; uu < 16; ++uu)
-                        tc_mma(dcol, a0 + 8 * uu, bdesc0 + uu * (kBTile / 16), idesc, (uu == 0 && first) ? 0u : 1u,
-                               sfa, sfb);
+                        for (int uu = 0; uu < 16; ++uu)
+                            tc_mma_ss(dcol, ad0 + (uint64_t)(uu * (4096 / 16)), bdesc0 + uu * (kBTile / 16), idesc,
+                                      (uu == 0 && first) ? 0u : 1u, sfa, sfb);
+                    } else {
+                        const uint32_t a0 = tmem + slot * 128;
+#pragma unroll
+                        for (int uu = 0; uu < 16; ++uu)
+                            tc_mma(dcol, a0 + 8 * uu, bdesc0 + uu * (kBTile / 16), idesc, (uu == 0 && first) ? 0u : 1u,
+                                   sfa, sfb);
+                    }
                     if (!p.resident) tc_commit(&bars.a_empty[slot]);
                 }
                 __syncwarp();
@@ -233,6 +247,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
         auto publish = [&]() {
             if (pend_slot >= 0) {
                 tmem_st_wait();
+                if (pend_slot >= p.slots) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // SMEM A
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.a_full[pend_slot]);
@@ -260,7 +275,17 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
                 const uint32_t t0 = wtile_s + (uint32_t)st0 * kWTileBytes;
                 const uint32_t t1 = wtile_s + (uint32_t)st1 * kWTileBytes;
                 const uint32_t dst = tmem + lane_off + (uint32_t)(slot * 128);
-                if (kind == 0)
+                if (p.resident && ps >= p.slots) {
+                    // A of this pass in SMEM: the row's line of the core matrices
+                    const uint32_t sdst = smem_u32(sa) + (uint32_t)(ps - p.slots) * 16u * 4096u +
+                                          (uint32_t)((m >> 3) * 256 + (m & 7) * 16);
+                    if (kind == 0)
+                        convert_pass<0, true>(t0, t1, swz, sdst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                    else if (kind == 1)
+                        convert_pass<1, true>(t0, t1, swz, sdst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                    else
+                        convert_pass<2, true>(t0, t1, swz, sdst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
+                } else if (kind == 0)
                     convert_pass<0>(t0, t1, swz, dst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
                 else if (kind == 1)
                     convert_pass<1>(t0, t1, swz, dst, 0u, sgn, 0, &bars.w_empty[st0], &bars.w_empty[st1], lane);
@@ -820,9 +845,15 @@ bool make_lplan(const LstmArgs& g, int npad, int sms, LPlan& p)
     if (p.slots < 2) return false;
     // A of every pass resident (converted once, at step 0) when it fits the A ring
     p.resident = (p.passes <= p.slots && !getenv_flag_off("PB_LSTM_RESIDENT")) ? 1 : 0;
-    if (p.resident) p.slots = p.passes;
+    p.spass = 0;
+    if (!p.resident && p.passes - p.slots <= kMaxSPass && !getenv_flag_off("PB_LSTM_RESIDENT") &&
+        !getenv_flag_off("PB_LSTM_SMEM_A")) {
+        p.resident = 1;                                         // the last passes' A in SMEM
+        p.spass = p.passes - p.slots;
+    }
+    if (p.resident && !p.spass) p.slots = p.passes;
     p.helpers = (p.resident && g.B == 1 && !(g.a & 1) && g.a <= 16 && !getenv_flag_off("PB_LSTM_HELPERS")) ? 1 : 0;
-    p.wstages = (int)((kSmemMax - lstm_fixed_smem(g.B, npad, p.chunks)) / kWTileBytes);
+    p.wstages = (int)((kSmemMax - lstm_fixed_smem(g.B, npad, p.chunks)) / kWTileBytes) - 4 * p.spass;
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     // >= 4: the two converter h-sets wait on the tiles of consecutive passes (2 tiles each); with
     // fewer stages a parity wait could see a barrier two phases behind it
@@ -855,7 +886,7 @@ cudaError_t launch_lt(const LstmArgs& g, cudaStream_t s)
     ga.L = g.L;
     CUtensorMap pmap, smap;
     if ((e = tc_weight_maps(ga, &pmap, &smap)) != cudaSuccess) return e;
-    const uint32_t smem = lstm_fixed_smem(g.B, NPAD, p.chunks) + (uint32_t)p.wstages * kWTileBytes;
+    const uint32_t smem = lstm_fixed_smem(g.B, NPAD, p.chunks) + (uint32_t)(p.wstages + 4 * p.spass) * kWTileBytes;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(p.tiles * p.chunks), 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);

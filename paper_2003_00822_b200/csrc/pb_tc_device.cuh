@@ -41,6 +41,16 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint32_t a_tmem, uint64_
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
         : "memory");
 }
+// The same with A from SMEM (descriptor a_desc, the layout of b_desc below).
+__device__ __forceinline__ void tc_mma_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate, uint32_t sfa, uint32_t sfb) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.scale_vec::2X [%0], %1, %2, %3, [%5], [%6], p;\n}\n" ::"r"(
+            d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+        : "memory");
+}
 // K-major, no swizzle: core matrix = 8 rows x 16 B; LBO = 128 B (K-adjacent),
 // SBO = 256 B (next 8 rows); version 1 (sm_100).
 __device__ __forceinline__ uint64_t b_desc(uint32_t saddr) {
@@ -159,7 +169,7 @@ __device__ __forceinline__ uint32_t sign_nibbles(uint32_t x, bool binary) {
 // swizzle: chunk c of row m at c ^ (m & 7)) and the stage goes back to the TMA
 // producer before its A registers are built and stored to TMEM (32 columns
 // per 4 chunks).
-template <int KIND>
+template <int KIND, bool SMEM = false>
 __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
                                              int sgn, int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
     constexpr bool kPair = KIND <= 1;
@@ -193,7 +203,20 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
                 for (int i = 0; i < 32; ++i) v[i] = sign_nibbles<KIND>(v[i], sgn == 2);
             }
             const int b4 = kPair ? 2 * t + h : h;
-            if (dbg != 1 && dbg != 3)
+            if (SMEM) {
+                // A in SMEM for an SS MMA (K-major, no swizzle, the layout of b_desc): dst is this
+                // row's core-matrix line; MMA uu = 4 b4 + j at uu * 4 KiB, its K halves 128 B apart
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t ad = dst + (uint32_t)((4 * b4 + j) * 4096);
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ad), "r"(v[8 * j]), "r"(v[8 * j + 1]),
+                                 "r"(v[8 * j + 2]), "r"(v[8 * j + 3])
+                                 : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ad + 128u), "r"(v[8 * j + 4]),
+                                 "r"(v[8 * j + 5]), "r"(v[8 * j + 6]), "r"(v[8 * j + 7])
+                                 : "memory");
+                }
+            } else if (dbg != 1 && dbg != 3)
                 st_tmem_x32(dst + (uint32_t)(32 * b4), v);
             else if (v[0] == 0x12345 && v[3] == 0x777)
                 asm volatile("trap;");   // keep the ALU work alive

@@ -9,7 +9,7 @@ rng = np.random.default_rng(1)
 Wih = (rng.standard_normal((4 * H, H)) / math.sqrt(H)).astype(np.float32)
 Whh = (rng.standard_normal((4 * H, H)) / math.sqrt(H)).astype(np.float32)
 bb = (0.1 * rng.standard_normal(4 * H)).astype(np.float32)
-for L, B in [(2, 1), (4, 1), (8, 1), (16, 1), (4, 4), (4, 16)]:
+for L, B in [tuple(map(int, c.split(','))) for c in os.environ.get("CFGS", "2,1 4,1 6,1 8,1 10,1 16,1 4,4 8,4 4,16").split()]:
     wi = pb.PackedWeights.quantize_device(torch.from_numpy(pb.interleave_gates(Wih)).cuda(), L)
     wh = pb.PackedWeights.quantize_device(torch.from_numpy(pb.interleave_gates(Whh)).cuda(), L)
     xs = torch.randn(T, B, H, device="cuda")

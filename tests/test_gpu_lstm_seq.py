@@ -52,7 +52,11 @@ def persist(request):
     (4, 1, 1100, 256, 4, 4, "auto"),     # W_hh K = 1100: 2 chunks, every tile split over 2 CTAs
     (3, 16, 512, 128, 4, 6, "auto"),     # batch 16: 128 digit columns (wide), 3 passes
     (3, 2, 2048, 256, 4, 4, "auto"),     # the LSTM-LM shape (H = 2048): 128 CTAs
-    (3, 5, 300, 200, 5, 7, "auto"),      # odd L, ragged tiles, a 4-row tail tile
+    (3, 5, 300, 200, 5, 7, "auto"),      # odd L, ragged tiles, a 4-row tail tile; 4 passes: A of the
+                                         # last in SMEM (persistent kernel)
+    (4, 1, 2048, 256, 4, 8, "auto"),     # LSTM-LM shape, L = 8: 3 passes' A in TMEM + 1 in SMEM
+    (3, 1, 512, 128, 4, 10, "auto"),     # L = 10: 2 passes' A in SMEM
+    (3, 4, 256, 128, 4, 9, "auto"),      # odd L = 9, batch 4: the canonical last layer's A in SMEM
 ])
 def test_lstm_seq(pb, torch, orc, persist, T, B, H, E, L_ih, L_hh, engine):
     s = synth.seed(7, T + 10 * B + H + E)
