@@ -712,7 +712,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // software pipeline: a pass's TMEM stores drain while the next pass's tiles are awaited
         int pend_slot = -1;
         int npub = 0;
-        bool hold = g.x != nullptr, converted = false;
+        bool hold = g.x != nullptr && !(p.dbg & 64), converted = false;
         auto publish = [&]() {
             if (pend_slot >= 0) {
                 tmem_st_wait();
