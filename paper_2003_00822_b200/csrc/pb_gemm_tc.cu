@@ -160,6 +160,9 @@ struct TcPlan {
     int dbg;          // profiling knob (env PB_TC_DEBUG): 1 = no A store, 2 = no MMA, 3 = neither,
                       // 6 = per-CTA timeline
     int prof;         // env PB_TC_PROF: print wait-cycle totals of CTA 0
+    int local;        // fused path, one unit per CTA: its only B chunk is built in place, so no
+                      // grid-wide B slices, no grid barrier; the sign correction uses the chunk's
+                      // own sum of x_q (the correction is linear in the chunks)
 };
 
 // Units [u0, u1) of work item `item`: the static schedule splits the units evenly over
@@ -294,7 +297,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     // publishes the slices for the later chunks then overlaps the first chunk's build
     int k = 0;
 #pragma unroll 1
-    for (uint32_t it = i0 + ew; it < i1; it += kEpiWarps, ++k) {
+    for (uint32_t it = i0 + ew; it < (p.local ? i0 : i1); it += kEpiWarps, ++k) {
         const uint32_t b = it / Wt;
         const uint32_t w = it - b * Wt;
         const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
@@ -346,6 +349,15 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         } else {
 #pragma unroll   // (indexed registers: no local-memory array)
             for (int k = 0; k < kCx; ++k) u[k] = (uint32_t)act_cast(v[k], f, g.a);
+        }
+        if (p.local) {
+            // the chunk's sum of x_q for column b (codes fit 32 bits: a <= 32)
+            long long xs = 0;
+#pragma unroll
+            for (int k = 0; k < kCx; ++k) xs += (int32_t)u[k];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) xs += __shfl_xor_sync(0xffffffffu, xs, o);
+            if (lane == 0) atomicAdd(&bars.xs[b], (unsigned long long)xs);
         }
         const long long c1 = kTimeline ? clock64() : 0;
         if (shfl) {
@@ -406,6 +418,12 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     if (pt == 0) {
         mbar_arrive(&bars.b_full[0]);
         mbar_arrive(&bars.pro_done);
+    }
+    if (p.local) {
+        // the chunk sums (bar 5 above ordered the atomics) are the epilogue's x_q sums
+        if (pt < B) bars.xsum[pt] = bars.xs[pt];
+        asm volatile("bar.sync 5, 128;" ::: "memory");
+        if (pt == 0) mbar_arrive(&bars.x_ready);
     }
     if TLP(g) tc0 = gtimer();
     if (TLP(g) && et == 0) {
@@ -581,7 +599,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         if (!g.x) pdl_wait();
         bool published = false;
         auto wait_published = [&]() {
-            if (g.x && !published) {
+            if (g.x && !p.local && !published) {
                 mbar_wait(&bars.slice_done, 0);                        // this CTA's slice is written
                 // the CTA's slice writes are ordered before the arrival by the epilogue warps'
                 // bar.sync + slice_done mbarrier and the cumulative release of the arrival
@@ -827,7 +845,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // a5: y = dequant(acc) (+ bias, + y when accumulating), then fn -- or, in cell mode
         // (pb_lstm_seq), the LSTM cell over the 4 gate rows of a hidden unit (lanes 4j..4j+3)
         auto preact = [&](int b, int64_t row, unsigned long long t) -> float {
-            t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
+            if (!p.local) t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
             const long long accv = (long long)t;
             const int64_t o = (int64_t)b * g.R + row;
             if (g.acc) g.acc[o] = accv;
@@ -1019,6 +1037,18 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.d_empty[db]);
+                if (p.local) {
+                    // local mode: this chunk's (o - |S_0|) sum x_q joins the segment's partial
+                    const unsigned long long x0 = xsum_of(0);
+                    if (!kWide && g.B == 1) {
+                        tot1 += o_corr * x0;
+                    } else {
+                        for (int b = 0; b < nb; ++b) {
+                            const uint32_t sa = s_tot_s + (uint32_t)(b * kTcRows + m) * 8u;
+                            st_shared_u64(sa, ld_shared_u64(sa) + o_corr * bars.xsum[b0 + b]);
+                        }
+                    }
+                }
                 stage_cols(b0, nb, seg & 1);
                 seg_b0 = b0;
                 spar = seg & 1;
@@ -1357,6 +1387,7 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     if (e != cudaSuccess) return e;
     p.dbg = dbg;
     p.prof = prof;
+    p.local = (g.x && p.stat && NPAD <= kTcMaxN && p.units <= p.gs && p.items == p.gs && !(dbg & 128)) ? 1 : 0;
     // weight ring: every 16 KiB stage the B stages and epilogue sums leave free
     p.bstages = (p.passes <= 2 && NPAD <= kTcMaxN) ? kMaxBStages : 2;
     if (bst_env) p.bstages = bst_env < 2 ? 2 : (bst_env > kMaxBStages ? kMaxBStages : bst_env);
