@@ -100,6 +100,7 @@ struct Bars {
     int fin_tile;                            // static schedule: shared tile this CTA completed (-1: none)
     uint64_t slice_done;                     // fused path: this CTA's slice of B written (epilogue warps)
     uint64_t pro_done;                       // fused path: first chunk's B built (converters resume)
+    uint64_t red_full;                       // local cluster mode (leader): the partners' sums arrived
     unsigned long long gbase;                // fused path: prologue grid-barrier counter base (grid_base)
     uint32_t tmem_base;
     int last_flag;
@@ -163,6 +164,8 @@ struct TcPlan {
     int local;        // fused path, one unit per CTA: its only B chunk is built in place, so no
                       // grid-wide B slices, no grid barrier; the sign correction uses the chunk's
                       // own sum of x_q (the correction is linear in the chunks)
+    int clu;          // local mode, 2..8 K-chunks: a tile's chunks are one thread-block cluster; the
+                      // partners st.async their exact sums into the leader's SMEM (rank 0)
 };
 
 // Units [u0, u1) of work item `item`: the static schedule splits the units evenly over
@@ -468,11 +471,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     uint8_t* wtile0 = smem + kHdrBytes;
     uint8_t* btile0 = wtile0 + p.wstages * kWTileBytes;
     const uint32_t s_tot_s = smem_u32(btile0 + p.bstages * kBStage);   // [b][128] u64 (B > 1)
+    const uint32_t redbuf_s = s_tot_s + (uint32_t)g.bs * kTcRows * 8u;   // [clu-1][b][128] u64 (leader)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long G = gridDim.x;
     long long prof[5] = {0, 0, 0, 0, 0};
     const long long g_start = gtimer();
+    bool cwaited = false;                      // local cluster mode: this thread waited the cluster barrier
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.slots; ++s) {
@@ -498,6 +503,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         mbar_init(&bars.x_ready, 1);
         mbar_init(&bars.slice_done, 1);
         mbar_init(&bars.pro_done, 1);
+        mbar_init(&bars.red_full, 1);
+        if (p.clu && blockIdx.x % p.clu == 0)   // the leader expects every partner's sums
+            mbar_arrive_expect_tx(&bars.red_full, (uint32_t)((p.clu - 1) * g.B * kTcRows * 8));
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(&pmap) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&smap) : "memory");
@@ -507,6 +515,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             smem_u32(&bars.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
+    // local cluster mode: every thread arrives once (the leader's barrier inits are published);
+    // the epilogue warps wait before their first DSMEM exchange, everyone else at the end
+    if (p.clu) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     // warp 0 (whose thread 0 initialised the barriers) only arrives: its weight tiles start
     // streaming now, while the other warps wait for the TMEM allocation and the scale factors
     if (warp == 0) {
@@ -1069,6 +1080,41 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         finish_tile_row(0, row, tot1);
                     else
                         finish_cols(b0, nb, row);
+                } else if (p.clu) {
+                    // local cluster mode: one chunk per CTA, the tile's chunks are the cluster
+                    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+                    if (kcA > 0) {
+                        const uint32_t rb = mapa_shared_u32(redbuf_s + (uint32_t)(((kcA - 1) * g.bs * kTcRows + m) * 8), 0);
+                        const uint32_t rbar = mapa_shared_u32(smem_u32(&bars.red_full), 0);
+                        for (int b = 0; b < nb; ++b) {
+                            const unsigned long long v = (!kWide && g.B == 1) ? tot1
+                                : ld_shared_u64(s_tot_s + (uint32_t)(b * kTcRows + m) * 8u);
+                            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                                             rb + (uint32_t)(b * kTcRows * 8)),
+                                         "l"(v), "r"(rbar)
+                                         : "memory");
+                        }
+                    } else {
+                        asm volatile(
+                            "{\n.reg .pred p;\nWC_%=:\nmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], 0;\n"
+                            "@!p bra WC_%=;\n}\n" ::"r"(smem_u32(&bars.red_full))
+                            : "memory");
+                        const int64_t row = (int64_t)rt * kTcRows + m;
+                        if (!kWide && g.B == 1) {
+                            for (int r = 1; r < p.clu; ++r) tot1 += ld_shared_u64(redbuf_s + (uint32_t)(((r - 1) * g.bs * kTcRows + m) * 8));
+                            finish_tile_row(0, row, tot1);
+                        } else {
+                            for (int b = 0; b < nb; ++b) {
+                                const uint32_t sa = s_tot_s + (uint32_t)(b * kTcRows + m) * 8u;
+                                unsigned long long t = ld_shared_u64(sa);
+                                for (int r = 1; r < p.clu; ++r)
+                                    t += ld_shared_u64(redbuf_s + (uint32_t)((((r - 1) * g.bs + b) * kTcRows + m) * 8));
+                                st_shared_u64(sa, t);
+                            }
+                            finish_cols(b0, nb, row);
+                        }
+                    }
+                    cwaited = true;
                 } else {
                     if (!kWide && g.B == 1) {
                         red_add_u64(ab, tot1);
@@ -1162,6 +1208,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             for (int k = 0; k < 10; ++k) r[k] = rec[k];
         }
     }
+    if (p.clu && !cwaited) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (TLP(g) && warp == 1 && lane == 0) {
@@ -1323,11 +1370,13 @@ cudaError_t weight_maps_cached(const GemmArgs& g, int dev, CUtensorMap* pmap, CU
 template <int NPAD>
 cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
 {
-    static int dbg = -1, prof = 0, bst_env = 0, stat_env = -1, dyn_pct = 0;
+    static int dbg = -1, prof = 0, bst_env = 0, stat_env = -1, dyn_pct = 0, clu_max = 4;   // 8-CTA clusters: 1.6x slower (co-scheduling)
     static std::once_flag env_once;
     std::call_once(env_once, [] {
         const char* ev = getenv("PB_TC_DEBUG");
         dbg = ev ? atoi(ev) : 0;
+        ev = getenv("PB_TC_CLU");              // experiment knob: largest local-mode cluster (< 2: off)
+        if (ev) clu_max = atoi(ev);
         ev = getenv("PB_TC_KNOB");             // profiling knob with the timeline on (PB_TC_DEBUG=6)
         if (ev) dbg = atoi(ev);
         ev = getenv("PB_TC_PROF");
@@ -1388,11 +1437,13 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     p.dbg = dbg;
     p.prof = prof;
     p.local = (g.x && p.stat && NPAD <= kTcMaxN && p.units <= p.gs && p.items == p.gs && !(dbg & 128)) ? 1 : 0;
+    p.clu = (p.local && p.chunks >= 2 && p.chunks <= clu_max && p.gs % p.chunks == 0) ? p.chunks : 0;
     // weight ring: every 16 KiB stage the B stages and epilogue sums leave free
     p.bstages = (p.passes <= 2 && NPAD <= kTcMaxN) ? kMaxBStages : 2;
     if (bst_env) p.bstages = bst_env < 2 ? 2 : (bst_env > kMaxBStages ? kMaxBStages : bst_env);
     if (NPAD > kTcMaxN && p.bstages > 2) p.bstages = 2;        // 64 KiB per wide B stage
-    const uint32_t fixed = 1024 + kHdrBytes + (uint32_t)p.bstages * (kChunkWords / 2) * NPAD * 32 + (uint32_t)g.bs * kTcRows * 8;
+    const uint32_t fixed = 1024 + kHdrBytes + (uint32_t)p.bstages * (kChunkWords / 2) * NPAD * 32 + (uint32_t)g.bs * kTcRows * 8 +
+                           (uint32_t)(p.clu ? p.clu - 1 : 0) * g.bs * kTcRows * 8;
     p.wstages = (int)((kSmemMax - fixed) / kWTileBytes);
     if (p.wstages > kMaxWStages) p.wstages = kMaxWStages;
     if (p.wstages < 4) return cudaErrorNotSupported;
@@ -1405,11 +1456,15 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     cfg.blockDim = dim3(kThreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute la[1];
+    cudaLaunchAttribute la[2];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = 1;
+    la[1].id = cudaLaunchAttributeClusterDimension;             // local cluster mode: a tile's chunks
+    la[1].val.clusterDim.x = (unsigned)(p.clu ? p.clu : 1);
+    la[1].val.clusterDim.y = 1;
+    la[1].val.clusterDim.z = 1;
     cfg.attrs = la;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = p.clu ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, bitgemm_tc_kernel<NPAD>, g, p, pmap, smap);
 }
 
