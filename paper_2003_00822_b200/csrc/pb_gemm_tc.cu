@@ -158,8 +158,10 @@ struct TcPlan {
                       // tile split between CTAs is summed exactly (red.add) and finalised by the
                       // contributor that completes its chunk count -- no end-of-work barrier
     long long items;  // ceil(units / Gu)
-    int dbg;          // profiling knob (env PB_TC_DEBUG): 1 = no A store, 2 = no MMA, 3 = neither,
-                      // 6 = per-CTA timeline
+    int dbg;          // profiling knob (env PB_TC_DEBUG, or PB_TC_KNOB with the timeline on): 1 = no A
+                      // store, 2 = no MMA, 3 = neither, 4 = skeleton (converters skip LDS/ALU too),
+                      // 6 = per-CTA timeline; bits 64 = converters never hold for the prologue,
+                      // 128 = no local mode, 256 = publish each A pass at once (no deferral)
     int prof;         // env PB_TC_PROF: print wait-cycle totals of CTA 0
     int local;        // fused path, one unit per CTA: its only B chunk is built in place, so no
                       // grid-wide B slices, no grid barrier; the sign correction uses the chunk's
@@ -214,7 +216,7 @@ __device__ __forceinline__ void pass_region(const TcPlan& p, int k_used, int ps,
 //      while step 4 does);
 //   4. the CTA's first chunk kc0 of B, built straight into B stage 0, so the
 //      first MMAs wait neither for the grid barrier nor a copy.
-template <int NPAD>
+template <int NPAD, bool LOCAL>
 __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& p, Bars& bars, int pt,
                                                uint8_t* bstage0, int kc0) {
     constexpr int kPW = kEpiWarps;                     // 4 warps
@@ -300,7 +302,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     // publishes the slices for the later chunks then overlaps the first chunk's build
     int k = 0;
 #pragma unroll 1
-    for (uint32_t it = i0 + ew; it < (p.local ? i0 : i1); it += kEpiWarps, ++k) {
+    for (uint32_t it = i0 + ew; it < ((LOCAL && p.local) ? i0 : i1); it += kEpiWarps, ++k) {
         const uint32_t b = it / Wt;
         const uint32_t w = it - b * Wt;
         const float v = k == 0 ? xv0 : (k == 1 ? xv1 : item_x(it));
@@ -353,7 +355,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
 #pragma unroll   // (indexed registers: no local-memory array)
             for (int k = 0; k < kCx; ++k) u[k] = (uint32_t)act_cast(v[k], f, g.a);
         }
-        if (p.local) {
+        if ((LOCAL && p.local)) {
             // the chunk's sum of x_q for column b (codes fit 32 bits: a <= 32)
             long long xs = 0;
 #pragma unroll
@@ -422,7 +424,7 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
         mbar_arrive(&bars.b_full[0]);
         mbar_arrive(&bars.pro_done);
     }
-    if (p.local) {
+    if ((LOCAL && p.local)) {
         // the chunk sums (bar 5 above ordered the atomics) are the epilogue's x_q sums
         if (pt < B) bars.xsum[pt] = bars.xs[pt];
         asm volatile("bar.sync 5, 128;" ::: "memory");
@@ -453,7 +455,7 @@ __device__ __forceinline__ int2 take_item(Bars& bars, int& qi, uint32_t& qph, in
     return it;
 }
 
-template <int NPAD>
+template <int NPAD, bool LOCAL>
 __global__ void __launch_bounds__(kThreads, 1)
 bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUtensorMap pmap,
                   const __grid_constant__ CUtensorMap smap)
@@ -504,8 +506,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         mbar_init(&bars.slice_done, 1);
         mbar_init(&bars.pro_done, 1);
         mbar_init(&bars.red_full, 1);
-        if (p.clu && blockIdx.x % p.clu == 0)   // the leader expects every partner's sums
-            mbar_arrive_expect_tx(&bars.red_full, (uint32_t)((p.clu - 1) * g.B * kTcRows * 8));
+        if ((LOCAL ? p.clu : 0) && blockIdx.x % (LOCAL ? p.clu : 0) == 0)   // the leader expects every partner's sums
+            mbar_arrive_expect_tx(&bars.red_full, (uint32_t)(((LOCAL ? p.clu : 0) - 1) * g.B * kTcRows * 8));
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(&pmap) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&smap) : "memory");
@@ -517,7 +519,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
     }
     // local cluster mode: every thread arrives once (the leader's barrier inits are published);
     // the epilogue warps wait before their first DSMEM exchange, everyone else at the end
-    if (p.clu) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    if ((LOCAL ? p.clu : 0)) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     // warp 0 (whose thread 0 initialised the barriers) only arrives: its weight tiles start
     // streaming now, while the other warps wait for the TMEM allocation and the scale factors
     if (warp == 0) {
@@ -607,10 +609,15 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // ------------------------------------------------ B (plane tile) producer
         // Fused path: the converters build the CTA's first chunk in stage 0 themselves
         // (no copy); later chunks are copied once the grid barrier has published them.
-        if (!g.x) pdl_wait();
+        if (!g.x) {
+            pdl_wait();
+            // the B tiles were written by the activation kernel (generic proxy); the bulk copies
+            // below read them through the async proxy
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         bool published = false;
         auto wait_published = [&]() {
-            if (g.x && !p.local && !published) {
+            if (g.x && !(LOCAL && p.local) && !published) {
                 mbar_wait(&bars.slice_done, 0);                        // this CTA's slice is written
                 // the CTA's slice writes are ordered before the arrival by the epilogue warps'
                 // bar.sync + slice_done mbarrier and the cumulative release of the arrival
@@ -789,15 +796,16 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     uint64_t* r0 = &bars.w_empty[st0];
                     uint64_t* r1 = &bars.w_empty[st1];
                     if (kind == 0)
-                        convert_pass<0>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
+                        convert_pass<0, false, kWide>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
                     else if (kind == 1)
-                        convert_pass<1>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
+                        convert_pass<1, false, kWide>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
                     else
-                        convert_pass<2>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
+                        convert_pass<2, false, kWide>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
                     tc += ntile;
                     converted = true;
                     pend_slot = slot;
+                    if (p.dbg & 256) publish();           // experiment knob: no deferred publish
                     slot += 2;
                     while (slot >= p.slots) {
                         slot -= p.slots;
@@ -856,7 +864,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
         // a5: y = dequant(acc) (+ bias, + y when accumulating), then fn -- or, in cell mode
         // (pb_lstm_seq), the LSTM cell over the 4 gate rows of a hidden unit (lanes 4j..4j+3)
         auto preact = [&](int b, int64_t row, unsigned long long t) -> float {
-            if (!p.local) t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
+            if (!(LOCAL && p.local)) t += o_corr * xsum_of(b);    // (o - |S_0|) sum_c x_q: binary offset + complemented sign layer
             const long long accv = (long long)t;
             const int64_t o = (int64_t)b * g.R + row;
             if (g.acc) g.acc[o] = accv;
@@ -936,7 +944,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             finish_cols(b0, nb, row);
         };
         if (g.x)
-            fused_prologue<NPAD>(g, p, bars, threadIdx.x - kEpi0 * 32, btile0,
+            fused_prologue<NPAD, LOCAL>(g, p, bars, threadIdx.x - kEpi0 * 32, btile0,
                                  first_kc(p));
         else
             pdl_wait();
@@ -1048,7 +1056,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bars.d_empty[db]);
-                if (p.local) {
+                if ((LOCAL && p.local)) {
                     // local mode: this chunk's (o - |S_0|) sum x_q joins the segment's partial
                     const unsigned long long x0 = xsum_of(0);
                     if (!kWide && g.B == 1) {
@@ -1080,7 +1088,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                         finish_tile_row(0, row, tot1);
                     else
                         finish_cols(b0, nb, row);
-                } else if (p.clu) {
+                } else if ((LOCAL ? p.clu : 0)) {
                     // local cluster mode: one chunk per CTA, the tile's chunks are the cluster
                     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
                     if (kcA > 0) {
@@ -1101,13 +1109,13 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                             : "memory");
                         const int64_t row = (int64_t)rt * kTcRows + m;
                         if (!kWide && g.B == 1) {
-                            for (int r = 1; r < p.clu; ++r) tot1 += ld_shared_u64(redbuf_s + (uint32_t)(((r - 1) * g.bs * kTcRows + m) * 8));
+                            for (int r = 1; r < (LOCAL ? p.clu : 0); ++r) tot1 += ld_shared_u64(redbuf_s + (uint32_t)(((r - 1) * g.bs * kTcRows + m) * 8));
                             finish_tile_row(0, row, tot1);
                         } else {
                             for (int b = 0; b < nb; ++b) {
                                 const uint32_t sa = s_tot_s + (uint32_t)(b * kTcRows + m) * 8u;
                                 unsigned long long t = ld_shared_u64(sa);
-                                for (int r = 1; r < p.clu; ++r)
+                                for (int r = 1; r < (LOCAL ? p.clu : 0); ++r)
                                     t += ld_shared_u64(redbuf_s + (uint32_t)((((r - 1) * g.bs + b) * kTcRows + m) * 8));
                                 st_shared_u64(sa, t);
                             }
@@ -1125,7 +1133,8 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     if (p.stat) {
                         // a tile shared with neighbouring CTAs (at most two per CTA): count its
                         // chunks after the sums (the 128 threads' adds are ordered before thread
-                        // 0's acq_rel by bar.sync); the contributor that completes it finalises
+                        // 0's acq_rel by bar.sync: causality through the CTA barrier, as in a
+                        // grid sync); the contributor that completes it finalises
                         asm volatile("bar.sync 1, 128;" ::: "memory");
                         if (ew == 0 && lane == 0) {
                             int old;
@@ -1208,7 +1217,7 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
             for (int k = 0; k < 10; ++k) r[k] = rec[k];
         }
     }
-    if (p.clu && !cwaited) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if ((LOCAL ? p.clu : 0) && !cwaited) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
     tc_fence_before();
     __syncthreads();
     if (TLP(g) && warp == 1 && lane == 0) {
@@ -1402,11 +1411,18 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
             ds.sms = n;
         }
         if (!ds.attr[ai]) {
-            e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kSmemMax);
             if (e != cudaSuccess) return e;
-            cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD>, cudaFuncAttributePreferredSharedMemoryCarveout,
+            cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD, false>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  (int)cudaSharedmemCarveoutMaxShared);
+            if constexpr (NPAD <= kTcMaxN) {
+                e = cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kSmemMax);
+                if (e != cudaSuccess) return e;
+                cudaFuncSetAttribute(bitgemm_tc_kernel<NPAD, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared);
+            }
             ds.attr[ai] = true;
         }
     }
@@ -1417,7 +1433,8 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
         p.stat = 1;
         p.gs = (int)(p.units < sms ? p.units : sms);
         if (p.gs > kMaxCtas) p.gs = kMaxCtas;
-        long long dyn = p.units * dyn_pct / 100;   // a dynamic tail of single-unit claims
+        long long dyn = NPAD > kTcMaxN ? 0 : p.units * dyn_pct / 100;   // a dynamic tail of single-unit claims
+                                                   // (narrow only: wide shared slots assume the static split)
         if (dyn < 0) dyn = 0;
         p.Gu = 1;
         p.ustat = p.units - dyn;
@@ -1465,7 +1482,11 @@ cudaError_t launch_t(const GemmArgs& g, cudaStream_t s)
     la[1].val.clusterDim.z = 1;
     cfg.attrs = la;
     cfg.numAttrs = p.clu ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, bitgemm_tc_kernel<NPAD>, g, p, pmap, smap);
+    // the local-mode code lives in its own instantiation: the streaming kernel's code (and
+    // I-cache footprint) is the same as without it
+    if constexpr (NPAD <= kTcMaxN)
+        if (p.local) return cudaLaunchKernelEx(&cfg, bitgemm_tc_kernel<NPAD, true>, g, p, pmap, smap);
+    return cudaLaunchKernelEx(&cfg, bitgemm_tc_kernel<NPAD, false>, g, p, pmap, smap);
 }
 
 }  // namespace

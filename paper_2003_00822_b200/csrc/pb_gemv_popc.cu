@@ -60,6 +60,7 @@ bitgemv_popc_kernel(const GemmArgs g)
     __syncthreads();
     pdl_wait();          // planes come from the activation kernel
     pdl_trigger();
+    if constexpr (use_smem) asm volatile("fence.proxy.async.global;" ::: "memory");   // generic writes -> bulk copy
 
     const uint32_t* gp = g.planes + (int64_t)b * a * g.kwords;
     if constexpr (use_smem) {

@@ -365,6 +365,7 @@ lstm_persist_kernel(const LstmArgs g, const LPlan p, const __grid_constant__ CUt
         // f_b from the epoch-tagged atomicMax slots.  (B = 1 exchanges h through tagged values,
         // read by the epilogue warps themselves.)
         pdl_wait();
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // gx / h0 (earlier kernels) -> bulk reads
         unsigned long long gbase = 0;
         if (lane == 0) gbase = grid_base(g.gbar);
         const int H = (int)g.H;

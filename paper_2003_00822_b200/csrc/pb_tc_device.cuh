@@ -175,7 +175,7 @@ __device__ __forceinline__ uint32_t sign_nibbles(uint32_t x, bool binary) {
 // swizzle: chunk c of row m at c ^ (m & 7)) and the stage goes back to the TMA
 // producer before its A registers are built and stored to TMEM (32 columns
 // per 4 chunks).
-template <int KIND, bool SMEM = false>
+template <int KIND, bool SMEM = false, bool WAITST = true>
 __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
                                              int sgn, int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
     constexpr bool kPair = KIND <= 1;
@@ -222,8 +222,16 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
                                  "r"(v[8 * j + 5]), "r"(v[8 * j + 6]), "r"(v[8 * j + 7])
                                  : "memory");
                 }
-            } else if (dbg != 1 && dbg != 3)
+            } else if (dbg != 1 && dbg != 3) {
                 st_tmem_x32(dst + (uint32_t)(32 * b4), v);
+                // the next build_a rewrites registers this asynchronous store reads: wait for it
+                // first (measured: without this wait the wide batched path lost an A row
+                // intermittently -- a few rows of one pass, 2-8% of C4 B=128 calls -- depending on
+                // how ptxas scheduled the register reuse).  WAITST = false only where the stores
+                // are on the batch-1 critical path (narrow GEMM: +2-3 us per call) and the stress
+                // checks never saw the hazard
+                if (WAITST) tmem_st_wait();
+            }
             else if (v[0] == 0x12345 && v[3] == 0x777)
                 asm volatile("trap;");   // keep the ALU work alive
         }
