@@ -39,7 +39,10 @@
 // CTA is summed exactly with red.add.u64 and finalised by the contributor that
 // completes its chunk count (atom.acq_rel), which also re-zeroes the sums and
 // the counter, so the workspace is left as it was found.  PB_TC_STATIC=0 selects
-// dynamic claims with an end-of-work grid barrier instead.
+// dynamic claims with an end-of-work grid barrier instead.  Local mode (LOCAL = true, its own
+// instantiation): with at most one unit per SM every CTA builds its only B chunk itself, so the
+// grid-wide B slices and their barrier are skipped, the sign correction uses the chunk's own
+// sum of x_q, and with 2-4 K-chunks the tile's chunks form a cluster that sums over DSMEM.
 //
 // Warp roles (15 warps, 480 threads, one CTA per SM):
 //   warp 0       schedule + weight producer: TMA (cp.async.bulk.tensor.3d, 128B
@@ -440,6 +443,20 @@ __device__ __forceinline__ void fused_prologue(const GemmArgs& g, const TcPlan& 
     }
 }
 
+#ifndef PB_NARROW_KA
+#define PB_NARROW_KA 1
+#endif
+// The converters' A build: the wide kernel waits each TMEM store; the batch-1 kernels alternate
+// two register sets (convert_pass_ka) so no store's source registers are rewritten early.
+template <int NPAD, int KIND>
+__device__ __forceinline__ void convert_pass_gemm(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
+                                                  int dbg, uint64_t* r0, uint64_t* r1, int lane) {
+    if constexpr (NPAD > kTcMaxN || !PB_NARROW_KA)
+        convert_pass<KIND, false, (NPAD > kTcMaxN)>(t0, t1, swz, dst, xm, 0, dbg, r0, r1, lane);
+    else
+        convert_pass_ka<KIND>(t0, t1, swz, dst, xm, dbg, r0, r1, lane);
+}
+
 // Reads work item `it` from the queue slot (qi, qph) and releases the slot (each
 // consuming warp arrives once).  Warp-uniform.
 __device__ __forceinline__ int2 take_item(Bars& bars, int& qi, uint32_t& qph, int lane) {
@@ -796,11 +813,11 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                     uint64_t* r0 = &bars.w_empty[st0];
                     uint64_t* r1 = &bars.w_empty[st1];
                     if (kind == 0)
-                        convert_pass<0, false, kWide>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
+                        convert_pass_gemm<NPAD, 0>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
                     else if (kind == 1)
-                        convert_pass<1, false, kWide>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
+                        convert_pass_gemm<NPAD, 1>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
                     else
-                        convert_pass<2, false, kWide>(t0, t1, swz, dst, xm, 0, p.dbg, r0, r1, lane);
+                        convert_pass_gemm<NPAD, 2>(t0, t1, swz, dst, xm, p.dbg, r0, r1, lane);
                     if (TLP(g) && warp == kConv0 && lane == 0 && pc == 0) bars.t_cv[2] = gtimer();
                     tc += ntile;
                     converted = true;

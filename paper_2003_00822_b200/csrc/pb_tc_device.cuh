@@ -227,15 +227,68 @@ __device__ __forceinline__ void convert_pass(uint32_t t0, uint32_t t1, uint32_t 
                 // the next build_a rewrites registers this asynchronous store reads: wait for it
                 // first (measured: without this wait the wide batched path lost an A row
                 // intermittently -- a few rows of one pass, 2-8% of C4 B=128 calls -- depending on
-                // how ptxas scheduled the register reuse).  WAITST = false only where the stores
-                // are on the batch-1 critical path (narrow GEMM: +2-3 us per call) and the stress
-                // checks never saw the hazard
+                // how ptxas scheduled the register reuse).  The batch-1 GEMM, where a wait per
+                // store costs 2-3 us per call, uses convert_pass_ka instead
                 if (WAITST) tmem_st_wait();
             }
             else if (v[0] == 0x12345 && v[3] == 0x777)
                 asm volatile("trap;");   // keep the ALU work alive
         }
     }
+}
+
+// tcgen05.wait::st that keeps the 32 source registers of the store it waits for live up to this
+// point, so the compiler cannot give them to other values while that store may still read them.
+__device__ __forceinline__ void tmem_st_wait_keep(const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.wait::st.sync.aligned;" ::"r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),
+        "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+        "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+// convert_pass for the batch-1 GEMM (TMEM destination, no sign nibbles): the 4 A stores of a
+// pass alternate two register sets; store k waits for store k - 1 (its registers kept live) after
+// building k's registers, so the build overlaps the previous store and no source register is
+// rewritten while a store may read it; one wait per pass is exposed (the last store's).
+template <int KIND>
+__device__ __forceinline__ void convert_pass_ka(uint32_t t0, uint32_t t1, uint32_t swz, uint32_t dst, uint32_t xm,
+                                                int dbg, uint64_t* rel0, uint64_t* rel1, int lane) {
+    constexpr bool kPair = KIND <= 1;
+    if (dbg == 4) {                             // profiling knob: the pipeline skeleton only
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(rel0);
+            if (kPair) mbar_arrive(rel1);
+        }
+        return;
+    }
+    const bool store = dbg != 1 && dbg != 3;
+    uint32_t va[32], vb[32];
+#pragma unroll
+    for (int t = 0; t < (kPair ? 2 : 1); ++t) {
+        uint4 q[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) q[c] = lds128((t == 0 ? t0 : t1) + ((((uint32_t)c) ^ swz) << 4));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(t == 0 ? rel0 : rel1);
+#pragma unroll
+        for (int h = 0; h < (kPair ? 2 : 4); ++h) {
+            const int k = kPair ? 2 * t + h : h;              // store index (compile time)
+            uint32_t(&v)[32] = (k & 1) ? vb : va;
+            if (kPair) {
+                const uint4 qq[4] = {q[4 * h], q[4 * h + 1], q[4 * h + 2], q[4 * h + 3]};
+                build_a<KIND>(qq, xm, v);
+            } else {
+                const uint4 qq[4] = {q[2 * h], q[2 * h + 1], q[2 * h], q[2 * h + 1]};
+                build_a<KIND>(qq, xm, v);
+            }
+            if (k > 0) tmem_st_wait_keep((k & 1) ? va : vb);
+            if (store) st_tmem_x32(dst + (uint32_t)(32 * k), v);
+            else if (v[0] == 0x12345 && v[3] == 0x777) asm volatile("trap;");
+        }
+    }
+    tmem_st_wait_keep(vb);                                    // the last store (k = 3)
 }
 
 // Least significant layer of pass ps (the pass's unit weight is |S_lo|).
