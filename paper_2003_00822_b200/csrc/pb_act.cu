@@ -162,13 +162,14 @@ cudaError_t launch_act_quant(const float* x, int64_t B, int64_t K, int64_t kword
                              int act_frac, void* ws, const WsLayout& l, cudaStream_t s)
 {
     if (B == 0 || kwords == 0) return cudaSuccess;
-    static bool carveout = false;
-    if (!carveout) {
+    static bool carveout[64] = {};                // per device (a function attribute is per context)
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !carveout[dev]) {
         // keep the SM in its max-shared-memory configuration between this kernel and
         // the tensor-engine GEMM (which needs 162 KiB): no L1/SMEM repartition per launch
         cudaFuncSetAttribute(act_quant_transpose_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              (int)cudaSharedmemCarveoutMaxShared);
-        carveout = true;
+        carveout[dev] = true;
     }
     char* base = static_cast<char*>(ws);
     const int nsplit = act_nsplit(kwords);

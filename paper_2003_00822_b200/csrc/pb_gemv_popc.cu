@@ -16,6 +16,7 @@
 // the plane scales T_j into a wrapping 64-bit sum, then weighted by S_i;
 // the per-lane partials are reduced with 64-bit warp shuffles.
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include "pb_common.cuh"
@@ -25,6 +26,7 @@ namespace pb {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMaxDevices = 64;               // per-device launch state
 constexpr int kWarps = kThreads / 32;
 constexpr uint32_t kMaxSmemPlanes = 160 * 1024;
 
@@ -162,29 +164,35 @@ cudaError_t launch_t2(const GemmArgs& g, cudaStream_t s)
 {
     const uint32_t plane_bytes = (uint32_t)(g.a * g.kwords * 4);
     const size_t smem = use_smem ? plane_bytes : 0;
-    static bool attr_set = false;
-    cudaError_t e;
-    if (!attr_set) {
+    // per-device launch state (the function attribute and the SM count are per device/context;
+    // occupancy depends only on the dynamic smem size: the last query is cached)
+    struct State {
+        bool attr_set = false;
+        int sms = 0, occ = 1;
+        size_t last_smem = ~size_t(0);
+    };
+    static State st[kMaxDevices];
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu);
+    State& d = st[dev];
+    if (!d.attr_set) {
         e = cudaFuncSetAttribute(bitgemv_popc_kernel<APAD, use_smem>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmemPlanes);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        if ((e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        d.attr_set = true;
     }
-    // occupancy depends only on the dynamic smem size: cache the last query
-    static int sms = 0;
-    static size_t last_smem = ~size_t(0);
-    static int occ = 1;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    if (smem != last_smem) {
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, bitgemv_popc_kernel<APAD, use_smem>, kThreads, smem);
+    if (smem != d.last_smem) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d.occ, bitgemv_popc_kernel<APAD, use_smem>, kThreads, smem);
         if (e != cudaSuccess) return e;
-        if (occ < 1) occ = 1;
-        last_smem = smem;
+        if (d.occ < 1) d.occ = 1;
+        d.last_smem = smem;
     }
+    const int sms = d.sms, occ = d.occ;
     int64_t want = (g.R + kWarps - 1) / kWarps;
     int64_t cap = (int64_t)sms * occ / (g.B > 0 ? g.B : 1);
     if (cap < 1) cap = 1;
