@@ -152,6 +152,7 @@ struct TcPlan {
                       // when the stages cover it (units of 1-2 passes take ~0.5-1 us of MMAs)
     int passes;       // ceil(k_used / 2): layer pairs (0,1), (2,3), ...
     int Gp;           // passes per accumulator group (<= G/2 layers pairs, K * 2^G <= 2^24)
+    int dsingle;      // narrow with one accumulator set (as wide mode): see make_plan
     int regions;      // ceil(passes / Gp)
     int Gu;           // units per work item (dynamic claims)
     int gs;           // static schedule: grid size; ustat: units split statically (the rest is
@@ -701,9 +702,10 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 int ue = (gt + 1) * p.chunks;
                 if (ue > it.y) ue = it.y;
                 // narrow: D double-buffered by segment parity; wide: one D, drained per segment
-                const int db = kWide ? 0 : (seg & 1);
-                if (kWide ? seg >= 1 : seg >= 2)
-                    TWAIT(&bars.d_empty[db], (uint32_t)((kWide ? seg - 1 : (seg >> 1) - 1) & 1), 0);
+                const bool d1 = kWide || p.dsingle;     // one accumulator set
+                const int db = d1 ? 0 : (seg & 1);
+                if (d1 ? seg >= 1 : seg >= 2)
+                    TWAIT(&bars.d_empty[db], (uint32_t)((d1 ? seg - 1 : (seg >> 1) - 1) & 1), 0);
                 tc_fence_after();
                 const uint32_t dbase = tmem + (uint32_t)(p.d_col + db * p.regions * NPAD);
                 for (const int us = u; u < ue; ++u, ++cc) {
@@ -1000,8 +1002,9 @@ bitgemm_tc_kernel(const GemmArgs g, const TcPlan p, const __grid_constant__ CUte
                 int ue = (gt + 1) * p.chunks;
                 if (ue > it.y) ue = it.y;
                 const int kcB = kcA + (ue - u);
-                const int db = kWide ? 0 : (seg & 1);
-                mbar_wait(&bars.d_full[db], (uint32_t)((kWide ? seg : (seg >> 1)) & 1));
+                const bool d1 = kWide || p.dsingle;
+                const int db = d1 ? 0 : (seg & 1);
+                mbar_wait(&bars.d_full[db], (uint32_t)((d1 ? seg : (seg >> 1)) & 1));
                 tc_fence_after();
                 long long te[4] = {0, 0, 0, 0}, tcy[3] = {0, 0, 0};
                 if TLP(g) {
@@ -1329,8 +1332,16 @@ bool make_plan(const GemmArgs& g, int npad, TcPlan& p)
     p.passes = (g.k_used + 1) / 2;
     p.regions = (p.passes + p.Gp - 1) / p.Gp;
     if (p.regions > kMaxRegions) return false;
-    // narrow: two accumulator sets (segment parity); wide: one
+    // narrow: two accumulator sets (segment parity); wide: one -- and narrow too when two
+    // sets would leave fewer than two A slots (several groups at a wide N, e.g. L = 16 at K =
+    // 2048 with 64 digit columns): a drained accumulator then blocks the next segment's MMAs,
+    // but one launch covers twice the batch columns
+    p.dsingle = 0;
     p.d_col = 512 - ((wide ? 1 : 2) * p.regions * npad + 31) / 32 * 32;
+    if (!wide && (p.d_col - 64) / 128 < 2 && p.regions > 1) {
+        p.dsingle = 1;
+        p.d_col = 512 - (p.regions * npad + 31) / 32 * 32;
+    }
     p.sf_col = p.d_col - 64;
     p.slots = p.sf_col / 128;
     if (p.slots > kMaxSlots) p.slots = kMaxSlots;
